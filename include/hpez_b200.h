@@ -1,0 +1,165 @@
+/*
+ * hpez_b200.h -- C ABI of the B200-native HPEZ hot path (libhpez_b200.so).
+ *
+ * Plain pointers and sizes only; no torch types.  Device pointers are CUDA
+ * global-memory pointers on the current device; `stream` is a cudaStream_t
+ * passed as void*.  Every entry point returns an hpez_status.
+ *
+ * Each entry point names the reference interface it replaces (the reference
+ * is the pure-Python package hpez 0.1.0, pkg/src/hpez/…).  The reference-side
+ * binding a maintainer would add is shown in INTEGRATION.md.
+ */
+#ifndef HPEZ_B200_H
+#define HPEZ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HPEZ_MAX_RANK 5 /* 4 grid axes + the tuner's stacked batch axis */
+
+typedef enum {
+    HPEZ_OK = 0,
+    HPEZ_CORRUPT_STREAM = 1,    /* errors.CorruptStream (interp.py:80-83)   */
+    HPEZ_OUTLIER_UNDERFLOW = 2, /* errors.OutlierUnderflow (quant.py:123)   */
+    HPEZ_BAD_ARGUMENT = 3,      /* ValueError (interp.py:453-456, plan.py)  */
+    HPEZ_CUDA_ERROR = 4,
+    HPEZ_EMPTY_INPUT = 5,       /* errors.EmptyInput (huffman.py:27)        */
+    HPEZ_INVALID_TABLE = 6,     /* errors.InvalidTable (huffman.py:69-74)   */
+    HPEZ_TRUNCATED = 7          /* errors.TruncatedStream (huffman.py:171)  */
+} hpez_status;
+
+enum { HPEZ_COMPRESS = 0, HPEZ_DECOMPRESS = 1 };
+/* quant.ROUND_NONE / ROUND_F32 / ROUND_INT (quant.py:27-29) */
+enum { HPEZ_ROUND_NONE = 0, HPEZ_ROUND_F32 = 1, HPEZ_ROUND_INT = 2 };
+/* storage of the working grid on the device */
+enum { HPEZ_WORK_F32 = 0, HPEZ_WORK_F64 = 1 };
+/* device code stream element type */
+enum { HPEZ_CODES_U16 = 0, HPEZ_CODES_I32 = 1 };
+
+/* One level of plan.LevelSpec (plan.py:94-98) with its LevelConfig
+ * (plan.py:54-66).  kernel = index into plan.KERNEL_VARIANTS (plan.py:25-31);
+ * paradigm 0 = PARADIGM_ONED, 1 = PARADIGM_MULTIDIM. */
+typedef struct {
+    int32_t stride;
+    int32_t kernel;
+    int32_t paradigm;
+    int32_t n_order;
+    int32_t axis_order[HPEZ_MAX_RANK];
+    double bound;
+} hpez_level;
+
+/* Arguments of interp.run_levels (interp.py:440-445) minus the arrays. */
+typedef struct {
+    int32_t rank;
+    int64_t dims[HPEZ_MAX_RANK];
+    uint32_t frozen_mask;        /* bit a set: axis a in frozen_axes */
+    int32_t direction;           /* HPEZ_COMPRESS / HPEZ_DECOMPRESS */
+    int32_t rounding;            /* HPEZ_ROUND_* */
+    int64_t radius;              /* 1 .. 2^30 */
+    int32_t n_levels;
+    const hpez_level *levels;    /* host, coarse to fine */
+    const double *md_alpha;      /* host, `rank` weights, NULL = all ones */
+    int32_t block_size;          /* 0 = no per-block table */
+    const uint8_t *block_table;  /* host (n_levels, n_blocks) u8 or NULL */
+    int32_t work_dtype;          /* HPEZ_WORK_F32 / HPEZ_WORK_F64 */
+    int32_t code_dtype;          /* HPEZ_CODES_U16 (radius <= 32768) / I32 */
+    int32_t with_stats;          /* PassStats (interp.py:89-118) wanted */
+} hpez_sweep_desc;
+
+typedef struct hpez_plan_s *hpez_plan;
+
+/* Build the commit schedule of run_levels for one geometry/config
+ * (interp.py:415-433 class enumeration, :322-411 commit split).  The plan
+ * owns its device metadata and scratch; one run at a time per plan. */
+int hpez_plan_create(const hpez_sweep_desc *desc, hpez_plan *out);
+int hpez_plan_destroy(hpez_plan plan);
+/* Number of codes the sweep produces / consumes (= points - anchors). */
+int64_t hpez_plan_num_codes(hpez_plan plan);
+int32_t hpez_plan_num_commits(hpez_plan plan);
+int32_t hpez_plan_num_launches(hpez_plan plan);
+
+/* Replaces interp.run_levels (interp.py:440-472).  `work` is updated in
+ * place.  Compress: writes codes[0 .. num_codes) and up to `outl_cap`
+ * outliers (f64, stream order).  Decompress: reads `codes_avail` codes and
+ * `outl_cap` outliers; fewer codes than the plan needs -> CORRUPT_STREAM.
+ * Stats (compress, with_stats plans): stat_err_sum/stat_count (device,
+ * n_levels) are accumulated like PassStats.record; stat_dense (device,
+ * n_levels * points doubles, zero-initialised) receives the dense error
+ * grids.  Launches are asynchronous on `stream`; call hpez_sweep_finish. */
+int hpez_sweep_run(hpez_plan plan, void *work, void *codes, int64_t codes_avail,
+                   double *outliers, int64_t outl_cap, double *stat_err_sum,
+                   int64_t *stat_count, double *stat_dense, void *stream);
+/* Synchronise `stream`, report the outlier count (compress: produced, may
+ * exceed outl_cap -> rerun with a larger buffer; decompress: consumed) and
+ * the sweep status (OUTLIER_UNDERFLOW on an exhausted outlier stream). */
+int hpez_sweep_finish(hpez_plan plan, void *stream, int64_t *n_outliers);
+
+/* Replaces lorenzo.lorenzo_pass (lorenzo.py:145-179) on a device grid.
+ * Compress writes codes[N] and outliers; decompress reads them. */
+int hpez_lorenzo(int32_t rank, const int64_t *dims, int32_t work_dtype, void *work,
+                 double bound, int64_t radius, int32_t order, int32_t direction,
+                 int32_t rounding, int32_t code_dtype, void *codes, int64_t n_codes,
+                 double *outliers, int64_t outl_cap, int64_t *n_outliers, void *stream);
+
+/* np.bincount(codes) of huffman.encode (huffman.py:151): counts[0..nbins). */
+int hpez_histogram(const void *codes, int32_t code_dtype, int64_t n, uint32_t *counts,
+                   int64_t nbins, void *stream);
+
+/* huffman.code_lengths + canonical_codes (huffman.py:19-88), host side.
+ * freqs/lengths/values are host arrays of n symbols. */
+int hpez_huffman_table(const int64_t *freqs, int64_t n, uint8_t *lengths, uint64_t *values);
+
+/* Bit count of the packed payload: sum(lengths[codes]) (huffman.py:154).
+ * `lengths` is a device u8 table; result written to *nbits after a sync. */
+int hpez_huffman_nbits(const void *codes, int32_t code_dtype, int64_t n,
+                       const uint8_t *lengths_dev, int64_t *nbits, void *stream);
+
+/* huffman._pack_bits (huffman.py:91-113): MSB-first canonical bit packing
+ * of n codes into `out` (device, 4-byte aligned, ceil(nbits/32)*4 bytes).
+ * max_len = longest code length in the table (1..64). */
+int hpez_huffman_pack(const void *codes, int32_t code_dtype, int64_t n,
+                      const uint8_t *lengths_dev, const uint64_t *values_dev,
+                      int32_t max_len, uint8_t *out, int64_t nbits, void *stream);
+
+/* huffman._unpack_symbols (huffman.py:116-141), host table-driven decoder.
+ * Writes `count` symbols (int32) to out; returns TRUNCATED / INVALID_TABLE. */
+int hpez_huffman_decode(const uint8_t *payload, int64_t nbytes, const uint8_t *lengths,
+                        int64_t n_lengths, int64_t count, int32_t *out);
+
+/* tuner.tune_blocks scoring core (tuner.py:446-474): per complete block and
+ * candidate, the pairwise sums of |orig - pred| of the centred sub-block at
+ * bound 0, then the first-minimum argmin per (mini level, block).
+ * `grid` is the device field (work_dtype), `origins` host (n_full, rank)
+ * sub-block origins, candidates host hpez_level-style configs over the
+ * batch-shifted axes.  Writes winners (mini_levels, n_full) int32 (device). */
+typedef struct {
+    int32_t kernel;
+    int32_t paradigm;
+    int32_t n_order;
+    int32_t axis_order[HPEZ_MAX_RANK];
+} hpez_candidate;
+
+int hpez_tune_blocks(int32_t rank, const int64_t *dims, int32_t work_dtype, const void *grid,
+                     int32_t rounding, int32_t sub, int32_t mini_stride, int64_t n_full,
+                     const int64_t *origins_dev, uint32_t frozen_mask,
+                     const double *md_alpha, int32_t n_cand, const hpez_candidate *cands,
+                     int32_t *winners_dev, double *err_sums_dev, void *stream);
+
+/* Per-level code stream boundaries: out[0..n_levels] (n_levels + 1 entries),
+ * level li owns codes [out[li], out[li+1]) -- PassStats.code_chunks. */
+int hpez_plan_level_codes(hpez_plan plan, int64_t *out);
+
+/* Select the CUDA device for subsequent calls from this host thread. */
+int hpez_set_device(int32_t device);
+
+/* Library build information (arch string) for provenance checks. */
+const char *hpez_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

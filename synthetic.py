@@ -69,7 +69,7 @@ def grf(dims, slope, seed=0, device=None) -> np.ndarray:
     k = _kmag(dims, np)
     with np.errstate(divide="ignore"):
         amp = np.where(k > 0, k ** (slope / 2.0), 0.0)
-    f = np.fft.irfftn(spec * amp, s=dims)
+    f = np.fft.irfftn(spec * amp, s=dims, axes=tuple(range(len(dims))))
     f = (f - f.mean()) / f.std()
     return f.astype(np.float32)
 
