@@ -130,24 +130,11 @@ int hpez_huffman_pack(const void *codes, int32_t code_dtype, int64_t n,
 int hpez_huffman_decode(const uint8_t *payload, int64_t nbytes, const uint8_t *lengths,
                         int64_t n_lengths, int64_t count, int32_t *out);
 
-/* tuner.tune_blocks scoring core (tuner.py:446-474): per complete block and
- * candidate, the pairwise sums of |orig - pred| of the centred sub-block at
- * bound 0, then the first-minimum argmin per (mini level, block).
- * `grid` is the device field (work_dtype), `origins` host (n_full, rank)
- * sub-block origins, candidates host hpez_level-style configs over the
- * batch-shifted axes.  Writes winners (mini_levels, n_full) int32 (device). */
-typedef struct {
-    int32_t kernel;
-    int32_t paradigm;
-    int32_t n_order;
-    int32_t axis_order[HPEZ_MAX_RANK];
-} hpez_candidate;
-
-int hpez_tune_blocks(int32_t rank, const int64_t *dims, int32_t work_dtype, const void *grid,
-                     int32_t rounding, int32_t sub, int32_t mini_stride, int64_t n_full,
-                     const int64_t *origins_dev, uint32_t frozen_mask,
-                     const double *md_alpha, int32_t n_cand, const hpez_candidate *cands,
-                     int32_t *winners_dev, double *err_sums_dev, void *stream);
+/* tuner.tune_blocks scoring reduction (tuner.py:470-472): out[r] = numpy's
+ * pairwise sum of rows[r, 0..rowlen) (= rows.sum(axis=1) bit for bit).  The
+ * dense error grids come from bound-0 hpez_sweep_run trials with stats. */
+int hpez_rows_pairwise_sum(const double *rows, int64_t nrows, int64_t rowlen, double *out,
+                           void *stream);
 
 /* Per-level code stream boundaries: out[0..n_levels] (n_levels + 1 entries),
  * level li owns codes [out[li], out[li+1]) -- PassStats.code_chunks. */

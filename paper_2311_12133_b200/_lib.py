@@ -39,11 +39,6 @@ class SweepDesc(ctypes.Structure):
                 ("with_stats", ctypes.c_int32)]
 
 
-class Candidate(ctypes.Structure):
-    _fields_ = [("kernel", ctypes.c_int32), ("paradigm", ctypes.c_int32),
-                ("n_order", ctypes.c_int32), ("axis_order", ctypes.c_int32 * MAX_RANK)]
-
-
 _lib = None
 
 
@@ -73,10 +68,9 @@ def lib():
         "hpez_histogram": (I32, [P, I32, I64, P, I64, P]),
         "hpez_huffman_table": (I32, [P, I64, P, P]),
         "hpez_huffman_nbits": (I32, [P, I32, I64, P, ctypes.POINTER(I64), P]),
-        "hpez_huffman_pack": (I32, [P, I32, I64, P, P, P, I64, P]),
+        "hpez_huffman_pack": (I32, [P, I32, I64, P, P, I32, P, I64, P]),
         "hpez_huffman_decode": (I32, [P, I64, P, I64, I64, P]),
-        "hpez_tune_blocks": (I32, [I32, P, I32, P, I32, I32, I32, I64, P, U32, P, I32, P,
-                                   P, P, P]),
+        "hpez_rows_pairwise_sum": (I32, [P, I64, I64, P, P]),
         "hpez_set_device": (I32, [I32]),
         "hpez_build_info": (ctypes.c_char_p, []),
     }

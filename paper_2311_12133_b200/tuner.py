@@ -1,0 +1,549 @@
+"""Auto-tuning (§6 of the paper) with every trial sweep on the GPU.
+
+Mirrors the reference's tuner.py stage by stage so the chosen configuration
+-- and therefore the archive -- is identical: sampled per-axis statistics
+(tuner.py:86-133), global kernel/paradigm selection (:280-302), dimension
+freezing (:319-348), (alpha, beta) search (:351-374), the Lorenzo check
+(:385-402, :552-568) and the per-block table (:414-486).
+
+What moved to the device: every ``run_block_trial`` sweep (the native
+sweep with PassStats), the Lorenzo trials, and the block-table scoring
+(one stacked bound-0 sweep per candidate with dense error grids, then a
+per-block numpy-order pairwise reduction kernel).  Scalar decisions
+(entropy of codes, argmins, scores) stay in host numpy on the exact
+GPU-produced codes and sums, so ties break exactly as in the reference.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .device import bind, device, ptr, stream
+from .errors import GridTooSmall
+from .grid import ScalarGrid, axis_sampling_reach, sample_indices
+from .interp import TRAVERSAL_FVFI, codes_to_int32, f32_exact, run_levels_device
+from .plan import (DEFAULT_ANCHOR_STRIDE, KERNEL_VARIANTS, PARADIGM_MULTIDIM, PARADIGM_ONED,
+                   CompressionConfig, InterpKernel, KernelTag, LevelConfig, active_axes_of,
+                   anchor_count, build_level_plan, encode_tag, order_candidates)
+from .quant import DEFAULT_RADIUS, ROUND_F32, ROUND_NONE, rounding_for_kind
+
+TUNING_BLOCK_EXTENT = 65
+OUTLIER_BITS = 64.0
+ZERO_VARIANCE_EPS = 1e-30
+
+
+@dataclass(frozen=True)
+class QualityTarget:
+    kind: str = "ratio"
+    lam: float = 0.0
+
+    def __post_init__(self):
+        if self.kind not in ("ratio", "psnr"):
+            raise ValueError(f"unknown target {self.kind!r}")
+        if self.lam < 0:
+            raise ValueError(f"lambda must be >= 0, got {self.lam}")
+
+
+@dataclass(frozen=True)
+class TunerOptions:
+    """Search knobs; defaults of tuner.py:47-68."""
+
+    sample_rate: float = 0.002
+    block_size: int = 32
+    anchor_stride: int = DEFAULT_ANCHOR_STRIDE
+    radius: int = DEFAULT_RADIUS
+    lorenzo_coef: float = 1.2
+    alpha_set: tuple = (1.0, 1.25, 1.5, 1.75, 2.0)
+    beta_set: tuple = (1.5, 2.0, 3.0, 4.0)
+    kernel_set: str = "all"
+    use_natural: bool = True
+    use_md: bool = True
+    use_same_level: bool = True
+    use_freeze: bool = True
+    use_eb: bool = True
+    use_lorenzo: bool = True
+    use_blockwise: bool = True
+    traversal: str = TRAVERSAL_FVFI
+
+    def __post_init__(self):
+        if self.kernel_set not in ("linear", "cubic", "all"):
+            raise ValueError(f"unknown kernel set {self.kernel_set!r}")
+
+
+@dataclass(frozen=True)
+class SampleStats:
+    linear_mse: tuple
+    cubic_mse: tuple
+    freeze_candidate: int
+    sigma_sq: tuple
+    n_samples: int
+
+
+@dataclass(frozen=True)
+class MdWeights:
+    sigma_sq: tuple
+    alpha: tuple
+    combined_variance: float
+
+
+def md_weights(sigma_sq) -> MdWeights:
+    """Inverse-variance blend weights over 2..4 axes (kernels.py:165-188)."""
+    sig = tuple(float(s) for s in sigma_sq)
+    if not 2 <= len(sig) <= 4:
+        raise ValueError(f"need 2..4 axes, got {len(sig)}")
+    if any(s < 0 or not np.isfinite(s) for s in sig):
+        raise ValueError(f"variances must be finite and >= 0, got {sig}")
+    for i, s in enumerate(sig):
+        if s <= ZERO_VARIANCE_EPS:
+            return MdWeights(sig, tuple(1.0 if j == i else 0.0 for j in range(len(sig))), 0.0)
+    inv = np.array([1.0 / s for s in sig], dtype=np.float64)
+    total = float(inv.sum())
+    return MdWeights(sig, tuple(float(w / total) for w in inv), min(1.0 / total, min(sig)))
+
+
+_CUBIC = ((-3, -1.0 / 16), (-1, 9.0 / 16), (1, 9.0 / 16), (3, -1.0 / 16))
+
+
+def analyze_samples(grid: ScalarGrid, rate: float = 0.002) -> SampleStats:
+    """Per-axis linear / cubic prediction MSE on the strided sample
+    (tuner.py:86-124); numpy ufunc order kept so MSEs are bit-identical."""
+    idx = sample_indices(grid, rate)
+    data = grid.data
+    vals = data[tuple(idx.T)].astype(np.float64)
+    lin, cub, measured = [], [], []
+    for ax in range(grid.rank):
+        reach = axis_sampling_reach(grid.dims[ax])
+        if reach is None:
+            lin.append(math.nan)
+            cub.append(math.nan)
+            continue
+
+        def nb(off, ax=ax):
+            j = idx.copy()
+            j[:, ax] += off
+            return data[tuple(j.T)].astype(np.float64)
+
+        lmse = float(np.mean((vals - 0.5 * (nb(-1) + nb(1))) ** 2))
+        lin.append(lmse)
+        if reach >= 3:
+            # sum() over arrays starts from int 0: 0 + t0 + t1 + ... elementwise
+            pc = sum(c * nb(o) for o, c in _CUBIC)
+            cub.append(float(np.mean((vals - pc) ** 2)))
+        else:
+            cub.append(lmse)
+        measured.append(ax)
+    worst = max((cub[a] for a in measured), default=1.0)
+    sig = [cub[a] if a in measured else max(worst, 1.0) for a in range(grid.rank)]
+    freeze = max(measured, key=lambda a: cub[a])
+    return SampleStats(tuple(lin), tuple(cub), int(freeze), tuple(sig), len(idx))
+
+
+def blend_weights_f32(stats: SampleStats) -> tuple:
+    if len(stats.sigma_sq) < 2:
+        return ()
+    return tuple(float(np.float32(a)) for a in md_weights(stats.sigma_sq).alpha)
+
+
+# ------------------------------------------------------------------ trials --
+@dataclass
+class TrialResult:
+    level_mae: np.ndarray
+    codes: np.ndarray
+    n_coded: int
+    n_outliers: int
+    mse: float
+    value_range: float
+    stats: object = None
+
+
+def tuning_block(grid: ScalarGrid, extent: int = TUNING_BLOCK_EXTENT) -> np.ndarray:
+    sel = []
+    for ext in grid.dims:
+        size = min(ext, extent)
+        lo = (ext - size) // 2
+        sel.append(slice(lo, lo + size))
+    return grid.data[tuple(sel)].astype(np.float64)
+
+
+class _DeviceBlock:
+    """A tuning block resident in HBM with its pristine copy, reused by every
+    trial of one tune() call."""
+
+    def __init__(self, block: np.ndarray, rounding: int):
+        dev = device()
+        self.host = block
+        self.f32 = rounding == ROUND_F32 and f32_exact(block)
+        self.orig = torch.from_numpy(block.astype(np.float32) if self.f32 else block).to(dev)
+        self.work = torch.empty_like(self.orig)
+
+
+def run_block_trial(block, bound: float, configs, *, alpha: float = 1.0, beta: float = 1.0,
+                    frozen_dim=None, md_alpha=None, radius: int = DEFAULT_RADIUS,
+                    anchor_stride: int = DEFAULT_ANCHOR_STRIDE, traversal: str = TRAVERSAL_FVFI,
+                    extra_frozen=(), rounding: int = ROUND_NONE, dense: bool = False,
+                    want_work: bool = False) -> TrialResult:
+    """tuner.run_block_trial (tuner.py:160-185) on the GPU.  ``block`` is a
+    host array or a _DeviceBlock; returns the same TrialResult fields."""
+    dblk = block if isinstance(block, _DeviceBlock) else _DeviceBlock(np.asarray(block), rounding)
+    shape = dblk.host.shape
+    plan = build_level_plan(shape, anchor_stride, bound, alpha, beta, frozen_dim, configs)
+    frozen = set(extra_frozen)
+    if frozen_dim is not None:
+        frozen.add(frozen_dim)
+    alpha_vec = np.ones(len(shape)) if md_alpha is None else np.asarray(md_alpha)
+    dev = dblk.orig.device
+    nl = len(plan.levels)
+    st = {"err_sum": torch.zeros(nl, dtype=torch.float64, device=dev),
+          "count": torch.zeros(nl, dtype=torch.int64, device=dev),
+          "dense": torch.zeros((nl,) + tuple(shape), dtype=torch.float64, device=dev) if dense else None}
+    dblk.work.copy_(dblk.orig)
+    codes, outl, n_out = run_levels_device(
+        dblk.work, plan.levels, direction="compress", radius=radius, frozen_axes=tuple(sorted(frozen)),
+        md_alpha=alpha_vec, rounding=rounding, stats=st)
+    err_sum = st["err_sum"].cpu().numpy()
+    count = st["count"].cpu().numpy()
+    mae = np.array([float(err_sum[i] / count[i]) if count[i] else 0.0 for i in range(nl)])
+    codes_np = codes_to_int32(codes) if not dense else None
+    mse = rng = math.nan
+    if want_work:
+        w = dblk.work.cpu().numpy().astype(np.float64)
+        mse = float(np.mean((w - dblk.host) ** 2))
+        rng = float(dblk.host.max() - dblk.host.min())
+    res = TrialResult(mae, codes_np, int(codes.numel()), int(n_out), mse, rng)
+    res.stats = st
+    return res
+
+
+def _entropy_bits(codes: np.ndarray) -> float:
+    if codes.size == 0:
+        return 0.0
+    _, counts = np.unique(codes, return_counts=True)
+    p = counts / codes.size
+    return float(-(p * np.log2(p)).sum())
+
+
+def _coded_bit_rate(codes: np.ndarray, n_outliers: int) -> float:
+    n = codes.size
+    if n == 0:
+        return 0.0
+    return _entropy_bits(codes) + OUTLIER_BITS * n_outliers / n
+
+
+def est_bit_rate(trial: TrialResult, elem_bits: int, anchor_fraction: float) -> float:
+    r = _coded_bit_rate(trial.codes, trial.n_outliers)
+    return (1.0 - anchor_fraction) * r + anchor_fraction * elem_bits
+
+
+def est_cr(trial: TrialResult, elem_bits: int, anchor_fraction: float) -> float:
+    rate = est_bit_rate(trial, elem_bits, anchor_fraction)
+    return math.inf if rate <= 0.0 else elem_bits / rate
+
+
+def _est_psnr(trial: TrialResult) -> float:
+    if trial.mse == 0.0 or trial.value_range == 0.0:
+        return math.inf
+    return 20.0 * math.log10(trial.value_range) - 10.0 * math.log10(trial.mse)
+
+
+def _target_score(trial, elem_bits, anchor_fraction, target: QualityTarget) -> float:
+    cr = est_cr(trial, elem_bits, anchor_fraction)
+    if target.kind == "ratio":
+        return cr
+    psnr = _est_psnr(trial)
+    if math.isinf(psnr):
+        return math.inf
+    return psnr + target.lam * math.log2(max(cr, 1e-300))
+
+
+def _anchor_fraction(dims, anchor_stride, frozen_dim) -> float:
+    return anchor_count(dims, anchor_stride, frozen_dim) / int(np.prod(np.asarray(dims, dtype=np.int64)))
+
+
+# ------------------------------------------------------------ candidates --
+def kernel_candidates(options: TunerOptions) -> list:
+    out = []
+    for kern in KERNEL_VARIANTS:
+        if kern.tag is not KernelTag.LINEAR:
+            if options.kernel_set == "linear":
+                continue
+            if kern.tag is KernelTag.CUBIC_NATURAL and (options.kernel_set != "all"
+                                                        or not options.use_natural):
+                continue
+            if kern.same_level and not options.use_same_level:
+                continue
+        out.append(kern)
+    return out
+
+
+def config_candidates(active, options: TunerOptions) -> list:
+    """Kernels outer, paradigms inner, cheapest first (tuner.py:260-270)."""
+    paradigms = [(PARADIGM_ONED, o) for o in order_candidates(active)]
+    if options.use_md and len(active) >= 2:
+        paradigms.append((PARADIGM_MULTIDIM, None))
+    return [LevelConfig(k, p, o) for k in kernel_candidates(options) for p, o in paradigms]
+
+
+def _n_levels(anchor_stride: int) -> int:
+    return max(anchor_stride.bit_length() - 1, 0)
+
+
+def _md_alpha_vec(md_alpha, rank: int) -> np.ndarray:
+    if md_alpha is None or len(md_alpha) == 0:
+        return np.ones(rank)
+    return np.asarray(md_alpha, dtype=np.float64)
+
+
+# ---------------------------------------------------------------- stages --
+def _block_of(grid, cache):
+    if cache is not None and "block" in cache:
+        return cache["block"]
+    b = _DeviceBlock(tuning_block(grid), rounding_for_kind(grid.kind))
+    if cache is not None:
+        cache["block"] = b
+    return b
+
+
+def tune_global(grid: ScalarGrid, stats: SampleStats, ebound: float, target: QualityTarget, *,
+                options: TunerOptions = TunerOptions(), frozen_dim=None, md_alpha=None,
+                _cache=None) -> list:
+    active = active_axes_of(grid.rank, frozen_dim)
+    cands = config_candidates(active, options)
+    block = _block_of(grid, _cache)
+    nl = _n_levels(options.anchor_stride)
+    alpha_vec = _md_alpha_vec(md_alpha, grid.rank)
+    maes = np.empty((len(cands), nl))
+    for ci, cand in enumerate(cands):
+        t = run_block_trial(block, 0.0, [cand] * nl, frozen_dim=frozen_dim, md_alpha=alpha_vec,
+                            radius=options.radius, anchor_stride=options.anchor_stride,
+                            traversal=options.traversal, rounding=rounding_for_kind(grid.kind))
+        maes[ci] = t.level_mae
+    return [cands[int(np.argmin(maes[:, li]))] for li in range(nl)]
+
+
+@dataclass(frozen=True)
+class FreezeDecision:
+    frozen_dim: int | None
+    configs: list
+    cr_frozen: float
+    cr_plain: float
+
+
+def tune_freeze(grid, stats, ebound, target, *, options: TunerOptions = TunerOptions(),
+                plain_configs=None, md_alpha=None, _cache=None) -> FreezeDecision:
+    if plain_configs is None:
+        plain_configs = tune_global(grid, stats, ebound, target, options=options,
+                                    md_alpha=md_alpha, _cache=_cache)
+    cand = stats.freeze_candidate
+    if grid.rank < 2 or not options.use_freeze:
+        return FreezeDecision(None, plain_configs, -math.inf, math.inf)
+    frozen_cfgs = tune_global(grid, stats, ebound, target, options=options, frozen_dim=cand,
+                              md_alpha=md_alpha, _cache=_cache)
+    block = _block_of(grid, _cache)
+    alpha_vec = _md_alpha_vec(md_alpha, grid.rank)
+    elem_bits = grid.kind.dtype.itemsize * 8
+    scores = []
+    for fd, cfgs in ((None, plain_configs), (cand, frozen_cfgs)):
+        t = run_block_trial(block, ebound, cfgs, frozen_dim=fd, md_alpha=alpha_vec,
+                            radius=options.radius, anchor_stride=options.anchor_stride,
+                            traversal=options.traversal, rounding=rounding_for_kind(grid.kind))
+        scores.append(est_cr(t, elem_bits, _anchor_fraction(grid.dims, options.anchor_stride, fd)))
+    cr_plain, cr_frozen = scores
+    if cr_frozen > cr_plain:
+        return FreezeDecision(cand, frozen_cfgs, cr_frozen, cr_plain)
+    return FreezeDecision(None, plain_configs, cr_frozen, cr_plain)
+
+
+def tune_eb(grid, ebound, target, *, options: TunerOptions = TunerOptions(), configs,
+            frozen_dim=None, md_alpha=None, _cache=None) -> tuple:
+    cands = [(1.0, 1.0)] + [(a, b) for a in options.alpha_set for b in options.beta_set]
+    block = _block_of(grid, _cache)
+    alpha_vec = _md_alpha_vec(md_alpha, grid.rank)
+    elem_bits = grid.kind.dtype.itemsize * 8
+    af = _anchor_fraction(grid.dims, options.anchor_stride, frozen_dim)
+    best, best_score = None, -math.inf
+    for a, b in cands:
+        t = run_block_trial(block, ebound, configs, alpha=a, beta=b, frozen_dim=frozen_dim,
+                            md_alpha=alpha_vec, radius=options.radius,
+                            anchor_stride=options.anchor_stride, traversal=options.traversal,
+                            rounding=rounding_for_kind(grid.kind),
+                            want_work=target.kind == "psnr")
+        score = _target_score(t, elem_bits, af, target)
+        if score > best_score:
+            best, best_score = (a, b), score
+    return best
+
+
+@dataclass(frozen=True)
+class LorenzoDecision:
+    predictor: str
+    order: int
+    rate_interp: float
+    rate_lorenzo: float
+
+
+def tune_lorenzo(grid, interp_rate: float, ebound: float, target, coefficient: float, *,
+                 options: TunerOptions = TunerOptions(), _cache=None) -> LorenzoDecision:
+    from .lorenzo import lorenzo_pass_device
+    block = _block_of(grid, _cache)
+    rounding = rounding_for_kind(grid.kind)
+    rates = []
+    for order in (1, 2):
+        block.work.copy_(block.orig)
+        codes, outl, n_out = lorenzo_pass_device(block.work, ebound, options.radius, order,
+                                                 direction="compress", rounding=rounding)
+        rates.append(_coded_bit_rate(codes_to_int32(codes), n_out))
+    best_order = 1 + int(np.argmin(rates))
+    best_rate = min(rates)
+    if interp_rate <= coefficient * best_rate:
+        return LorenzoDecision("interp", best_order, interp_rate, best_rate)
+    return LorenzoDecision("lorenzo", best_order, interp_rate, best_rate)
+
+
+def _sub_extent(block_size: int, rank: int) -> int:
+    return max(4, round(block_size * 0.04 ** (1.0 / rank)))
+
+
+def _pow2_at_most(n: int) -> int:
+    return 1 << max(n.bit_length() - 1, 0)
+
+
+def config_candidates_shifted(active, shifted_active, options):
+    orig = config_candidates(active, options)
+    shifted = config_candidates(shifted_active, options)
+    return [(sc, encode_tag(oc, active)) for sc, oc in zip(shifted, orig)]
+
+
+def _full_block_index(grid_shape, full_counts) -> np.ndarray:
+    coords = np.meshgrid(*[np.arange(c) for c in full_counts], indexing="ij")
+    flat = np.zeros(coords[0].size, dtype=np.int64)
+    for ax, c in enumerate(coords):
+        flat = flat * grid_shape[ax] + c.ravel()
+    return flat
+
+
+def row_pairwise_sums(rows) -> torch.Tensor:
+    """numpy ``rows.sum(axis=1)`` (pairwise order) of a 2-D f64 CUDA tensor."""
+    rows = rows.contiguous()
+    out = torch.empty(rows.shape[0], dtype=torch.float64, device=rows.device)
+    bind()
+    check(lib().hpez_rows_pairwise_sum(ptr(rows), rows.shape[0], rows.shape[1], ptr(out),
+                                       stream()), "hpez_rows_pairwise_sum")
+    return out
+
+
+def tune_blocks(grid: ScalarGrid, global_configs, ebound: float, *,
+                options: TunerOptions = TunerOptions(), frozen_dim=None, md_alpha=None):
+    """Per-block per-level tags (tuner.py:414-486).  Sub-blocks of every
+    complete block are stacked on a frozen batch axis; each candidate is one
+    bound-0 GPU sweep with dense error grids, reduced per block on the GPU
+    in numpy's pairwise order; argmin (first minimum) on the host."""
+    bs = options.block_size
+    rank = grid.rank
+    n_levels = _n_levels(options.anchor_stride)
+    active = active_axes_of(rank, frozen_dim)
+    grid_shape = tuple(-(-e // bs) for e in grid.dims)
+    n_blocks = int(np.prod(grid_shape))
+    full_counts = tuple(e // bs for e in grid.dims)
+    n_full = int(np.prod(full_counts))
+    global_tags = np.array([encode_tag(c, active) for c in global_configs], dtype=np.uint8)
+    table = np.tile(global_tags[:, None], (1, n_blocks))
+    if n_blocks <= 1 or n_full == 0 or len(active) == 0:
+        return None
+    sub = _sub_extent(bs, rank)
+    mini_stride = _pow2_at_most(max(sub - 1, 1))
+    if mini_stride < 2:
+        return None
+    lo = (bs - sub) // 2
+    starts = [np.arange(c) * bs + lo for c in full_counts]
+    mesh = np.meshgrid(*starts, indexing="ij")
+    origins = np.stack([m.ravel() for m in mesh], axis=1)
+    # gather the centred sub-blocks (host fancy index, then one upload)
+    idx = [origins[:, a][:, None] + np.arange(sub)[None, :] for a in range(rank)]
+    sel = tuple(idx[a].reshape((n_full,) + (1,) * a + (sub,) + (1,) * (rank - 1 - a))
+                for a in range(rank))
+    stacked = grid.data[sel].astype(np.float64)
+    rounding = rounding_for_kind(grid.kind)
+    dblk = _DeviceBlock(stacked, rounding)
+    shifted_active = tuple(1 + a for a in active)
+    cands = config_candidates_shifted(active, shifted_active, options)
+    alpha_vec = np.concatenate(([0.0], _md_alpha_vec(md_alpha, rank)))
+    extra_frozen = (0,) + ((1 + frozen_dim,) if frozen_dim is not None else ())
+    mini_levels = _n_levels(mini_stride)
+    err = torch.empty((len(cands), mini_levels, n_full), dtype=torch.float64, device=dblk.orig.device)
+    for ci, (cand, _) in enumerate(cands):
+        t = run_block_trial(dblk, 0.0, [cand] * mini_levels, md_alpha=alpha_vec,
+                            radius=options.radius, anchor_stride=mini_stride,
+                            traversal=options.traversal, extra_frozen=extra_frozen,
+                            rounding=rounding, dense=True)
+        dense = t.stats["dense"]
+        for li in range(mini_levels):
+            err[ci, li] = row_pairwise_sums(dense[li].reshape(n_full, -1))
+    winners = np.argmin(err.cpu().numpy(), axis=0)
+    level_offset = n_levels - mini_levels
+    full_index = _full_block_index(grid_shape, full_counts)
+    for mli in range(mini_levels):
+        fli = level_offset + mli
+        if fli < 0:
+            continue
+        table[fli, full_index] = np.array([cands[w][1] for w in winners[mli]], dtype=np.uint8)
+    return table
+
+
+def default_config(ebound: float, rank: int, options: TunerOptions = TunerOptions()) -> CompressionConfig:
+    """Untuned fallback: linear one-axis everywhere (tuner.py:510-519)."""
+    n_levels = _n_levels(options.anchor_stride)
+    cfg = LevelConfig(InterpKernel(KernelTag.LINEAR), PARADIGM_ONED, tuple(range(rank)))
+    return CompressionConfig(predictor="interp", resolved_bound=ebound, radius=options.radius,
+                             anchor_stride=options.anchor_stride, level_configs=(cfg,) * n_levels)
+
+
+def tune(grid: ScalarGrid, ebound: float, target: QualityTarget = QualityTarget(),
+         options: TunerOptions = TunerOptions()) -> CompressionConfig:
+    """Full search (tuner.py:522-579)."""
+    try:
+        stats = analyze_samples(grid, options.sample_rate)
+    except GridTooSmall:
+        return default_config(ebound, grid.rank, options)
+    cache: dict = {}
+    md_alpha = blend_weights_f32(stats) if options.use_md else ()
+    configs = tune_global(grid, stats, ebound, target, options=options, md_alpha=md_alpha,
+                          _cache=cache)
+    frozen_dim = None
+    if grid.rank >= 2 and options.use_freeze:
+        dec = tune_freeze(grid, stats, ebound, target, options=options, plain_configs=configs,
+                          md_alpha=md_alpha, _cache=cache)
+        frozen_dim = dec.frozen_dim
+        configs = dec.configs
+    alpha, beta = 1.0, 1.0
+    if options.use_eb:
+        alpha, beta = tune_eb(grid, ebound, target, options=options, configs=configs,
+                              frozen_dim=frozen_dim, md_alpha=md_alpha, _cache=cache)
+    if options.use_lorenzo:
+        block = _block_of(grid, cache)
+        t = run_block_trial(block, ebound, configs, alpha=alpha, beta=beta, frozen_dim=frozen_dim,
+                            md_alpha=_md_alpha_vec(md_alpha, grid.rank), radius=options.radius,
+                            anchor_stride=options.anchor_stride, traversal=options.traversal,
+                            rounding=rounding_for_kind(grid.kind))
+        elem_bits = grid.kind.dtype.itemsize * 8
+        af = _anchor_fraction(grid.dims, options.anchor_stride, frozen_dim)
+        dec = tune_lorenzo(grid, est_bit_rate(t, elem_bits, af), ebound, target,
+                           options.lorenzo_coef, options=options, _cache=cache)
+        if dec.predictor == "lorenzo":
+            return CompressionConfig(predictor="lorenzo", resolved_bound=ebound,
+                                     radius=options.radius, lorenzo_order=dec.order)
+    block_table = None
+    if options.use_blockwise:
+        block_table = tune_blocks(grid, configs, ebound, options=options, frozen_dim=frozen_dim,
+                                  md_alpha=md_alpha)
+    return CompressionConfig(
+        predictor="interp", resolved_bound=ebound, radius=options.radius,
+        anchor_stride=options.anchor_stride, alpha=alpha, beta=beta, frozen_dim=frozen_dim,
+        level_configs=tuple(configs), md_alpha=tuple(md_alpha),
+        block_size=options.block_size if block_table is not None else 0, block_table=block_table)

@@ -183,6 +183,29 @@ def tune_blocks_case(name, data, kind="f64", frozen=None, md=None, options=None)
     save(name, meta, **arrays)
 
 
+def samples_case(name, data, kind, rate=0.002):
+    grid = ScalarGrid(data.shape, ElementKind(kind), np.asarray(data).astype(ElementKind(kind).dtype))
+    st = tuner.analyze_samples(grid, rate)
+    w = tuner.blend_weights_f32(st)
+    meta = dict(kind="samples", grid_kind=kind, rate=rate, linear_mse=list(st.linear_mse),
+                cubic_mse=list(st.cubic_mse), freeze=st.freeze_candidate,
+                sigma_sq=list(st.sigma_sq), n=st.n_samples, weights=list(w))
+    save(name, meta, input=np.ascontiguousarray(grid.data))
+
+
+def tune_global_case(name, data, kind, e, frozen=None, options=None):
+    options = options or tuner.TunerOptions()
+    grid = ScalarGrid(data.shape, ElementKind(kind), np.asarray(data).astype(ElementKind(kind).dtype))
+    st = tuner.analyze_samples(grid, options.sample_rate)
+    md = tuner.blend_weights_f32(st)
+    cfgs = tuner.tune_global(grid, st, e, tuner.QualityTarget(), options=options,
+                             frozen_dim=frozen, md_alpha=md)
+    active = tuple(a for a in range(grid.rank) if a != frozen)
+    meta = dict(kind="tune_global", grid_kind=kind, bound=e, frozen=frozen, md=list(md),
+                tags=[int(encode_tag(c, active)) for c in cfgs])
+    save(name, meta, input=np.ascontiguousarray(grid.data))
+
+
 def pipeline_case(name, data, kind, mode, eps, options=None, config=None):
     grid = ScalarGrid(data.shape, ElementKind(kind), np.asarray(data).astype(ElementKind(kind).dtype))
     spec = ErrorBoundSpec(mode, eps)
@@ -338,6 +361,14 @@ def main():
     tune_blocks_case("tuneblk_frozen", f32(syn.patchwork((64, 40, 64), seed=3)), frozen=1, md=(0.2, 0.0, 0.8))
     tune_blocks_case("tuneblk_4d", f32(syn.patchwork((32, 17, 16, 33), seed=4)), md=(0.25, 0.25, 0.25, 0.25),
                      options=tuner.TunerOptions(block_size=16))
+    # --- sampled statistics and global selection (tuner.py:86-133, :280-302)
+    samples_case("samples_3d", syn.config_field(3, dims=(40, 64, 64)), "f32")
+    samples_case("samples_2d", syn.patchwork((96, 128), seed=6), "f64", rate=0.01)
+    samples_case("samples_small", syn.trig_product((5, 40, 2)), "f64", rate=0.05)
+    samples_case("samples_4d", syn.trig_product((12, 10, 9, 8), freq=0.7), "f64", rate=0.01)
+    tune_global_case("tglobal_3d", syn.config_field(2, dims=(70, 66, 72)), "f32", 1e-3)
+    tune_global_case("tglobal_frozen", syn.patchwork((64, 70, 64), seed=7), "f64", 1e-3, frozen=0)
+    tune_global_case("tglobal_2d", syn.trig_product((128, 128)), "f64", 1e-4)
     # --- whole pipeline archives (pipeline.py:57-143) -------------------------
     fast = tuner.TunerOptions(sample_rate=0.01)
     pipeline_case("pipe_f64_rel", syn.trig_product((70, 90)), "f64", BoundMode.REL, 1e-3, options=fast)
