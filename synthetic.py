@@ -58,11 +58,17 @@ def grf(dims, slope, seed=0, device=None) -> np.ndarray:
         import torch
         t = torch.from_numpy(noise).to(device)
         spec = torch.fft.rfftn(t)
-        k = _kmag(dims, torch.fft)
-        k = torch.as_tensor(k, device=device) if not torch.is_tensor(k) else k.to(device)
-        amp = torch.where(k > 0, k.clamp_min(1e-12) ** (slope / 2.0),
-                          torch.zeros_like(k))
-        f = torch.fft.irfftn(spec * amp, s=dims)
+        k2 = torch.zeros(spec.shape, dtype=torch.float32, device=t.device)
+        for a, d in enumerate(dims):
+            last = a == len(dims) - 1
+            k = (torch.fft.rfftfreq(d, device=t.device) if last
+                 else torch.fft.fftfreq(d, device=t.device)) * d
+            shape = [1] * len(dims)
+            shape[a] = k.shape[0]
+            k2 = k2 + (k * k).reshape(shape)
+        kk = torch.sqrt(k2)
+        amp = torch.where(kk > 0, kk.clamp_min(1e-12) ** (slope / 2.0), torch.zeros_like(kk))
+        f = torch.fft.irfftn(spec * amp, s=dims, dim=tuple(range(len(dims))))
         f = (f - f.mean()) / f.std()
         return f.float().cpu().numpy()
     spec = np.fft.rfftn(noise)
