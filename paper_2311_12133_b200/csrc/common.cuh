@@ -14,10 +14,8 @@
 namespace hpez {
 
 constexpr int kMaxRank = HPEZ_MAX_RANK;
-constexpr int kThreads = 256;          // threads per commit CTA
-constexpr int kItems = 4;              // lattice positions per thread
-constexpr int kBlockPos = kThreads * kItems;
-constexpr int kWarps = kThreads / 32;
+constexpr int kItemWarps = 8;              // warps per work item
+constexpr int kItemThreads = kItemWarps * 32;
 
 // ------------------------------------------------------------ fast divmod --
 // Division of u32 by a runtime constant (dividends < 2^31).
@@ -85,9 +83,10 @@ struct TagInfo {            // per block tag of a mixed class (interp.py:350-411
 struct GridDev {
     int32_t rank;
     int32_t block_size;
-    int64_t dims[kMaxRank];
-    int64_t estr[kMaxRank];     // element strides
-    int64_t bstr[kMaxRank];     // block-grid strides (row-major block index)
+    int32_t dims[kMaxRank];
+    int32_t estr[kMaxRank];     // element strides
+    int32_t bstr[kMaxRank];     // block-grid strides (row-major block index)
+    int32_t pad;
     int64_t npts;
     int64_t nblk;               // blocks per table level
     int64_t radius;
@@ -100,20 +99,24 @@ struct CommitDev {
     int32_t level;
     int32_t phase;
     uint32_t axes_present;      // mixed: split axes P
-    int64_t start[kMaxRank];
-    int64_t step[kMaxRank];
-    FastDiv cnt[kMaxRank];
+    int32_t start[kMaxRank];
+    int32_t step[kMaxRank];
+    int32_t cnt[kMaxRank];
+    FastDiv fd[kMaxRank];
     uint32_t npos;
-    uint32_t nblocks;
-    int64_t s;
+    int32_t s;
     double bound;
     double two_e;
-    int64_t code_base;          // uniform commits: first code index
-    int64_t blk_base;           // first ticket of this launch
+    double inv_two_e;           // fl(1 / two_e), quantizer fast path
+    int64_t code_base;          // uniform commits: code index of position 0
+    int32_t item_base;          // first global item id
+    int32_t n_items;
+    int32_t p_item;             // positions per item (multiple of 256)
+    int32_t pw;                 // positions per warp (p_item / 8)
     int32_t tag_off;            // mixed: TagInfo slot 0 of the class
     int32_t slot_off;           // mixed: 256-entry tag->slot map
     int32_t commit_id;
-    int32_t pad;
+    int32_t fast_id;            // rank-3 uniform specialisation, -1 = generic path
     PredDev pred;               // uniform commits
 };
 
@@ -128,17 +131,30 @@ __device__ __forceinline__ double round_native(double v) {
 
 // quant.quantize_block for one point (quant.py:80-105).  Returns the code;
 // *out is the decompressor-visible value (recon, or orig on escape).
+// The quotient x = (orig - pred) / (2e) is formed as a product with the
+// reciprocal; k = floor(|x| + 0.5) can only differ from the correctly rounded
+// division when |x| + 0.5 lies within a few ulps of an integer, in which case
+// the exact IEEE division decides.
 template <int ROUND>
 __device__ __forceinline__ int64_t quantize_point(double orig, double pred, double bound,
-                                                  double two_e, int64_t R, double *out) {
+                                                  double two_e, double inv_two_e, int64_t R,
+                                                  double *out) {
     double recon;
     bool ok;
     int64_t code;
     if (bound > 0.0) {
-        double x = __ddiv_rn(__dsub_rn(orig, pred), two_e);
-        double fl = floor(__dadd_rn(fabs(x), 0.5));
+        const double d = __dsub_rn(orig, pred);
+        double x = __dmul_rn(d, inv_two_e);
+        double y = __dadd_rn(fabs(x), 0.5);
+        double fl = floor(y);
+        const double fr = __dsub_rn(y, fl);
+        const double margin = __dmul_rn(y, 0x1p-40);
+        if (fr < margin || fr > __dsub_rn(1.0, margin)) {
+            x = __ddiv_rn(d, two_e);
+            fl = floor(__dadd_rn(fabs(x), 0.5));
+        }
         double k = x > 0.0 ? fl : (x < 0.0 ? -fl : 0.0);  // np.sign(x) * fl
-        bool inr = fabs(k) < (double)R;
+        const bool inr = fabs(k) < (double)R;
         if (!inr) k = 0.0;
         recon = round_native<ROUND>(__dadd_rn(pred, __dmul_rn(two_e, k)));
         ok = inr && (fabs(__dsub_rn(recon, orig)) <= bound);
@@ -156,91 +172,23 @@ __device__ __forceinline__ int64_t quantize_point(double orig, double pred, doub
 template <int ROUND>
 __device__ __forceinline__ double dequantize_point(double pred, int64_t code, double two_e,
                                                    int64_t R) {
-    double k = (double)(code - R);
+    const double k = (double)(code - R);
     return round_native<ROUND>(__dadd_rn(pred, __dmul_rn(two_e, k)));
 }
 
-// ----------------------------------------------------- block-wide ranking --
-// Exclusive ranks of flags ordered (item, thread) -- i.e. lattice position
-// order p = base + i*kThreads + tid -- and the block total.  smem needs
-// kItems*kWarps + 1 words.
-__device__ __forceinline__ void block_rank(const bool (&f)[kItems], uint32_t (&rank)[kItems],
-                                           uint32_t &total, uint32_t *smem) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int i = 0; i < kItems; i++) {
-        uint32_t m = __ballot_sync(0xffffffffu, f[i]);
-        rank[i] = __popc(m & lt);
-        if (lane == 0) smem[i * kWarps + warp] = __popc(m);
-    }
-    __syncthreads();
-    static_assert(kItems * kWarps <= 32, "single-warp scan");
-    if (warp == 0) {
-        uint32_t v = lane < kItems * kWarps ? smem[lane] : 0u;
-        uint32_t inc = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        if (lane < kItems * kWarps) smem[lane] = inc - v;
-        if (lane == 31) smem[kItems * kWarps] = inc;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kItems; i++) rank[i] += smem[i * kWarps + warp];
-    total = smem[kItems * kWarps];
-    __syncthreads();
+// ------------------------------------------------------ memory ordering --
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
-
-// ------------------------------------------------- decoupled look-back --
-// Ticket-ordered prefix of per-block counts across every launch of a sweep.
-constexpr uint64_t kFlagAgg = 1ull << 62;
-constexpr uint64_t kFlagInc = 2ull << 62;
-constexpr uint64_t kValMask = (1ull << 62) - 1;
-
-__device__ __forceinline__ uint64_t ld_volatile(const uint64_t *p) {
-    return *(const volatile uint64_t *)p;
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
 }
-__device__ __forceinline__ void st_volatile(uint64_t *p, uint64_t v) {
-    *(volatile uint64_t *)p = v;
-}
-
-// Called by all lanes of one warp.  Returns the exclusive prefix of block
-// `ticket` and publishes its inclusive value.
-__device__ __forceinline__ uint64_t lookback(uint64_t *status, uint64_t ticket, uint64_t agg) {
-    const int lane = threadIdx.x & 31;
-    if (ticket == 0) {
-        if (lane == 0) st_volatile(&status[0], kFlagInc | agg);
-        return 0;
-    }
-    if (lane == 0) st_volatile(&status[ticket], kFlagAgg | agg);
-    uint64_t excl = 0;
-    int64_t pos = (int64_t)ticket - 1;
-    while (true) {
-        int64_t q = pos - lane;
-        uint64_t w = kFlagInc;
-        if (q >= 0) {
-            do {
-                w = ld_volatile(&status[q]);
-            } while ((w >> 62) == 0);
-        }
-        uint32_t inc = __ballot_sync(0xffffffffu, (w >> 62) == 2);
-        uint64_t v = w & kValMask;
-        if (inc) {
-            int k = __ffs(inc) - 1;
-            if (lane > k) v = 0;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        excl += v;
-        if (inc) break;
-        pos -= 32;
-    }
-    __threadfence();
-    if (lane == 0) st_volatile(&status[ticket], kFlagInc | (excl + agg));
-    return excl;
+__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 }  // namespace hpez

@@ -1,26 +1,31 @@
 // sweep.cu -- B200 multi-level interpolation predict/quantize sweep and its
 // inverse: the drop-in for interp.run_levels (interp.py:440-472).
 //
-// Host side: a plan object restates the reference's commit schedule --
-// levels coarse to fine, parity classes combinations(active, m) in
-// lexicographic order (interp.py:415-433), uniform commits with the optional
-// same-level two-phase split (interp.py:322-341) and mixed per-block commits
-// A / B_phase (interp.py:350-411) -- and uploads it once.
+// Host side: a plan restates the reference's commit schedule -- levels
+// coarse to fine, parity classes combinations(active, m) in lexicographic
+// order (interp.py:415-433), uniform commits with the optional same-level
+// two-phase split (interp.py:322-341) and mixed per-block commits A / B_phase
+// (interp.py:350-411).  Every commit's lattice is cut into work items
+// (contiguous position ranges in row-major = stream order, 8 warps each).
 //
-// Device side: one launch per commit.  Each CTA owns a contiguous range of
-// lattice positions in row-major order (the order codes and outliers are
-// streamed in, interp.py:48-67), predicts every member from pre-commit state
-// with the resolved 1-D rows or the MD blend, quantizes / dequantizes in
-// f64 and writes the reconstruction in place.  Escapes are ranked with a
-// block-wide ballot scan plus a decoupled look-back chained across every
-// launch of the sweep, so outliers land in stream order without a second
-// pass.  Mixed commits get their member offsets from a data-independent
-// setup pass run once per plan.
+// Device side (one sweep = a handful of launches):
+//   * coarse kernel: one 1024-thread CTA runs the leading tiny commits back to
+//     back with __syncthreads between commits (no launch or flag latency);
+//   * flow kernel: a persistent grid pulls items in stream order from an
+//     atomic counter, waits on per-item completion flags of the previous
+//     commit's items within the stencil reach (+-3s along the outer axis),
+//     predicts/quantizes its positions and publishes its flag.  Commits thus
+//     pipeline plane by plane and the working set stays in the 126 MB L2;
+//   * escapes are counted per (item, warp): compress compacts the outliers in
+//     stream order afterwards (their originals are still in the grid),
+//     decompress ranks them with a counting pre-pass over the code stream.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <memory>
 #include <set>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -113,10 +118,7 @@ static cudaError_t upload_rows() {
         fam[f] = FamDesc{};
         fam[f].n = kFamN[f];
         for (int i = 0; i < kFamN[f]; i++) fam[f].u[i] = kFamU[f][i];
-        for (uint32_t m = 0; m < 64; m++) {
-            // a target always has its -1 neighbour (position >= stride)
-            rows[f][m] = (m < (1u << kFamN[f])) ? resolve(f, m) : RowEntry{};
-        }
+        for (uint32_t m = 0; m < 64; m++) rows[f][m] = (m < (1u << kFamN[f])) ? resolve(f, m) : RowEntry{};
     }
     cudaError_t e = cudaMemcpyToSymbol(c_rows, rows, sizeof rows);
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_fam, fam, sizeof fam);
@@ -124,287 +126,706 @@ static cudaError_t upload_rows() {
     return e;
 }
 
-// ------------------------------------------------------ device kernels --
-struct SweepPtrs {
-    void *work;
-    void *codes;
-    double *outl;
-    int64_t outl_cap;
-    uint64_t *status;
-    unsigned long long *ticket;
-    int32_t *flags;
-    const int64_t *blkoff;
+// ---------------------------------------------------------- predictions --
+template <typename T>
+__device__ __forceinline__ double ldv(const T *__restrict__ w, int64_t i) {
+    return (double)__ldcg(w + i);
+}
+
+#define DM(a, b) __dmul_rn((a), (b))
+#define DA(a, b) __dadd_rn((a), (b))
+
+// Generic row through the constant table (edges; any family).
+template <typename T>
+__device__ __noinline__ double pred_table(const T *__restrict__ w, int64_t idx, int c, int E, int s,
+                                          int64_t sE, int fam) {
+    const FamDesc &fd = c_fam[fam];
+    uint32_t mask = 0;
+    for (int i = 0; i < fd.n; i++) {
+        const int p = c + fd.u[i] * s;
+        mask |= (uint32_t)(p >= 0 && p < E) << i;
+    }
+    const RowEntry &r = c_rows[fam][mask];
+    double acc = DM(r.coef[0], ldv(w, idx + r.off[0] * sE));
+    for (int k = 1; k < r.n; k++) acc = DA(acc, DM(r.coef[k], ldv(w, idx + r.off[k] * sE)));
+    return acc;
+}
+
+// 1-D prediction at grid index idx, coordinate c along an axis of extent E,
+// stride s, element step sE = s * estr.  Interior points use the full row
+// with literal coefficients; edge points fall back to the resolved table.
+template <typename T>
+__device__ __forceinline__ double pred_1d(const T *__restrict__ w, int64_t idx, int c, int E, int s,
+                                          int64_t sE, int fam) {
+    switch (fam) {
+    case FAM_LIN_I:
+        if (c + s <= E - 1) return DA(DM(0.5, ldv(w, idx - sE)), DM(0.5, ldv(w, idx + sE)));
+        return DM(1.0, ldv(w, idx - sE));
+    case FAM_NAK_I:
+        if (c >= 3 * s && c + 3 * s <= E - 1) {
+            const double a = ldv(w, idx - 3 * sE), b = ldv(w, idx - sE), d = ldv(w, idx + sE),
+                         e = ldv(w, idx + 3 * sE);
+            return DA(DA(DA(DM(-1.0 / 16, a), DM(9.0 / 16, b)), DM(9.0 / 16, d)), DM(-1.0 / 16, e));
+        }
+        break;
+    case FAM_NAT_I:
+        if (c >= 3 * s && c + 3 * s <= E - 1) {
+            const double a = ldv(w, idx - 3 * sE), b = ldv(w, idx - sE), d = ldv(w, idx + sE),
+                         e = ldv(w, idx + 3 * sE);
+            return DA(DA(DA(DM(-3.0 / 40, a), DM(23.0 / 40, b)), DM(23.0 / 40, d)), DM(-3.0 / 40, e));
+        }
+        break;
+    case FAM_NAK_S:
+        if (c + 2 * s <= E - 1) {  // same-level targets sit at >= 3s
+            const double a = ldv(w, idx - 2 * sE), b = ldv(w, idx - sE), d = ldv(w, idx + sE),
+                         e = ldv(w, idx + 2 * sE);
+            return DA(DA(DA(DM(-1.0 / 6, a), DM(4.0 / 6, b)), DM(4.0 / 6, d)), DM(-1.0 / 6, e));
+        }
+        break;
+    default:  // FAM_NAT_S
+        if (c + 3 * s <= E - 1) {
+            const double a = ldv(w, idx - 3 * sE), b = ldv(w, idx - 2 * sE), d = ldv(w, idx - sE),
+                         e = ldv(w, idx + sE), f = ldv(w, idx + 2 * sE), h = ldv(w, idx + 3 * sE);
+            return DA(DA(DA(DA(DA(DM(3.0 / 62, a), DM(-18.0 / 62, b)), DM(46.0 / 62, d)),
+                            DM(46.0 / 62, e)), DM(-18.0 / 62, f)), DM(3.0 / 62, h));
+        }
+        break;
+    }
+    return pred_table(w, idx, c, E, s, sE, fam);
+}
+
+// Register copy of a predictor (uniform per warp for uniform commits).
+struct PredReg {
+    int md, axis, fam, nax;
+    int axes[kMaxRank];
+    double w[kMaxRank];
+};
+
+__device__ __forceinline__ PredReg load_pred(const PredDev &p) {
+    PredReg r;
+    r.md = p.md;
+    r.axis = p.axis;
+    r.fam = p.fam;
+    r.nax = p.nax;
+#pragma unroll
+    for (int i = 0; i < kMaxRank; i++) {
+        r.axes[i] = p.axes[i];
+        r.w[i] = p.w[i];
+    }
+    return r;
+}
+
+// arr[a] for a runtime-uniform a without local-memory indexing
+__device__ __forceinline__ int pick(const int (&arr)[kMaxRank], int a) {
+    int v = arr[0];
+#pragma unroll
+    for (int k = 1; k < kMaxRank; k++) v = a == k ? arr[k] : v;
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ double predict(const T *__restrict__ w, int64_t idx, const int (&coord)[kMaxRank],
+                                          const int (&dims)[kMaxRank], const int (&estr)[kMaxRank],
+                                          const PredReg &p, int s) {
+    if (!p.md) {
+        const int a = p.axis;
+        return pred_1d(w, idx, pick(coord, a), pick(dims, a), s, (int64_t)s * pick(estr, a), p.fam);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < kMaxRank; i++) {
+        if (i < p.nax) {
+            const int a = p.axes[i];
+            const double t = DM(p.w[i], pred_1d(w, idx, pick(coord, a), pick(dims, a), s,
+                                                (int64_t)s * pick(estr, a), p.fam));
+            acc = i == 0 ? t : DA(acc, t);
+        }
+    }
+    return acc;
+}
+
+// ------------------------------------------------------------ arguments --
+struct SweepArgs {
+    GridDev g;
+    const CommitDev *commits;
+    const int32_t *item_commit;
+    const int32_t *flow_order;    // flow items in grab order
+    const int32_t *dep_off;       // per item: first dependency interval
+    const int2 *dep_rng;          // item-id intervals (inclusive)
+    const int32_t *coarse_pairs;  // (commit, item) pairs of the coarse prefix
+    const int32_t *coarse_groups; // [g0, g1) pair ranges, one per (level, depth)
+    int32_t n_groups;
+    const int64_t *wbase;       // per (item, warp): code index of the first member
+    const int32_t *wn;          // per (item, warp): member count
+    uint32_t *esc_cnt;          // per (item, warp): escapes (compress, written)
+    const int64_t *esc_off;     // per (item, warp): first outlier rank (decompress)
+    uint32_t *done;             // per item completion flags
+    int32_t *next;              // flow item counter
+    int32_t *flags;             // status (outlier underflow)
     const TagInfo *tags;
     const uint8_t *slots;
     const uint8_t *table;
+    void *work;
+    void *codes;
+    const double *outl;
+    int64_t outl_cap;
     double *errbuf;
     double *dense;
+    int32_t n_items;            // flow kernel: number of items
 };
 
-template <typename T>
-__device__ __forceinline__ double predict_1d(const T *__restrict__ work, int64_t idx, int64_t c,
-                                             int64_t E, int64_t s, int64_t sE, int fam) {
-    const FamDesc &fd = c_fam[fam];
-    uint32_t mask = 0;
+// Position -> lattice indices (row-major).
+__device__ __forceinline__ void decode_pos(const CommitDev &cm, int rank, uint32_t p, int (&j)[kMaxRank]) {
 #pragma unroll
-    for (int i = 0; i < 6; i++) {
-        if (i < fd.n) {
-            int64_t p = c + (int64_t)fd.u[i] * s;
-            mask |= (uint32_t)(p >= 0 && p < E) << i;
+    for (int a = kMaxRank - 1; a >= 0; a--) {
+        if (a < rank) {
+            const uint32_t q = a > 0 ? fdiv(p, cm.fd[a]) : 0u;
+            j[a] = (int)(p - q * (uint32_t)cm.cnt[a]);
+            p = q;
         }
     }
-    const RowEntry &r = c_rows[fam][mask];
-    double acc = __dmul_rn(r.coef[0], (double)work[idx + (int64_t)r.off[0] * sE]);
-#pragma unroll
-    for (int k = 1; k < 6; k++) {
-        if (k < r.n)
-            acc = __dadd_rn(acc, __dmul_rn(r.coef[k], (double)work[idx + (int64_t)r.off[k] * sE]));
+}
+
+// Mixed-class membership and predictor of one position (interp.py:374-411).
+__device__ __forceinline__ const PredDev *mixed_member(const SweepArgs &A, const CommitDev &cm,
+                                                       const int (&coord)[kMaxRank], uint32_t jodd,
+                                                       bool *member) {
+    const GridDev &g = A.g;
+    int64_t b = 0;
+    for (int a = 0; a < g.rank; a++) b += (int64_t)(coord[a] / g.block_size) * g.bstr[a];
+    const int tag = A.table[(int64_t)cm.level * g.nblk + b];
+    const TagInfo &ti = A.tags[cm.tag_off + A.slots[cm.slot_off + tag]];
+    const int sp = ti.split;
+    if (cm.kind == COMMIT_MIXED_A) {
+        *member = sp < 0 || !((jodd >> sp) & 1u);
+        return &ti.inter;
     }
-    return acc;
+    const int key = __popc(cm.axes_present & jodd & ~(1u << (sp < 0 ? 31 : sp)));
+    *member = sp >= 0 && ((jodd >> sp) & 1u) && key == cm.phase;
+    return &ti.same;
 }
 
-template <typename T>
-__device__ __forceinline__ double predict(const GridDev &g, const T *__restrict__ work,
-                                          int64_t idx, const int32_t (&coord)[kMaxRank],
-                                          const PredDev &p, int64_t s) {
-    if (!p.md)
-        return predict_1d(work, idx, coord[p.axis], g.dims[p.axis], s, s * g.estr[p.axis], p.fam);
-    double acc = 0.0;
-    for (int i = 0; i < p.nax; i++) {
-        const int a = p.axes[i];
-        double t = __dmul_rn(p.w[i], predict_1d(work, idx, coord[a], g.dims[a], s, s * g.estr[a], p.fam));
-        acc = i == 0 ? t : __dadd_rn(acc, t);
+// One warp's share of one item: positions [p0, p0 + pw) of commit cm, in
+// stream order, 32 at a time.  Commit geometry and the predictor live in
+// registers; coordinates use static indexing only.
+template <typename T, typename C, int DIR, int ROUND, bool STATS>
+__device__ __forceinline__ void process_warp(const SweepArgs &A, const CommitDev &cmS, int item, int warp) {
+    const int lane = threadIdx.x & 31;
+    const int rank = A.g.rank;
+    const uint32_t npos = cmS.npos;
+    const uint32_t p0 = (uint32_t)(item - cmS.item_base) * (uint32_t)cmS.p_item + (uint32_t)warp * (uint32_t)cmS.pw;
+    const uint32_t pend = min(p0 + (uint32_t)cmS.pw, npos);
+    const int e = item * kItemWarps + warp;
+    if (p0 >= pend) {
+        if (DIR == HPEZ_COMPRESS && lane == 0) A.esc_cnt[e] = 0;
+        return;
     }
-    return acc;
-}
-
-template <typename C>
-__device__ __forceinline__ int64_t load_code(const C *codes, int64_t i) {
-    return (int64_t)codes[i];
-}
-
-template <typename T, typename C, int DIR, int ROUND, bool STATS, bool MIXED>
-__global__ void __launch_bounds__(kThreads) commit_kernel(const __grid_constant__ GridDev g,
-                                                          const __grid_constant__ CommitDev cm,
-                                                          const __grid_constant__ SweepPtrs P) {
-    __shared__ uint32_t s_rank[kItems * kWarps + 1];
-    __shared__ unsigned long long s_ticket;
-    __shared__ uint64_t s_excl;
-    if (threadIdx.x == 0) s_ticket = atomicAdd(P.ticket, 1ull);
-    __syncthreads();
-    const uint64_t ticket = s_ticket;
-    const uint32_t p0 = (uint32_t)(ticket - cm.blk_base) * (uint32_t)kBlockPos;
-    T *__restrict__ work = (T *)P.work;
-    C *__restrict__ codes = (C *)P.codes;
-    const int64_t R = g.radius;
-
-    int64_t idx[kItems];
-    int32_t coord[kItems][kMaxRank];
-    bool mem[kItems];
-    const PredDev *pp[kItems];
-    // pass 1: coordinates and membership
+    int st[kMaxRank], sp[kMaxRank], cn[kMaxRank], dims[kMaxRank], estr[kMaxRank];
 #pragma unroll
-    for (int i = 0; i < kItems; i++) {
-        const uint32_t pos = p0 + (uint32_t)(i * kThreads) + threadIdx.x;
-        mem[i] = pos < cm.npos;
-        uint32_t rem = mem[i] ? pos : 0u;
-        int64_t id = 0;
+    for (int a = 0; a < kMaxRank; a++) {
+        st[a] = cmS.start[a];
+        sp[a] = cmS.step[a];
+        cn[a] = cmS.cnt[a];
+        dims[a] = A.g.dims[a];
+        estr[a] = A.g.estr[a];
+    }
+    const int s = cmS.s;
+    const double bound = cmS.bound, two_e = cmS.two_e, inv_two_e = cmS.inv_two_e;
+    const int64_t R = A.g.radius;
+    const bool mixed = cmS.kind != COMMIT_UNIFORM;
+    const PredReg upred = load_pred(cmS.pred);
+    T *__restrict__ work = (T *)A.work;
+    C *__restrict__ codes = (C *)A.codes;
+    int64_t cbase = A.wbase[e];  // code index of this warp's first member
+    const int64_t obase = DIR == HPEZ_DECOMPRESS ? A.esc_off[e] : 0;
+    uint32_t nesc = 0;
+    int j[kMaxRank];
+    decode_pos(cmS, rank, p0 + lane, j);
+    const bool inc = cn[rank - 1] >= 32;
+    for (uint32_t pb = p0; pb < pend; pb += 32) {
+        const uint32_t p = pb + lane;
+        const bool valid = p < pend;
+        int coord[kMaxRank];
+        int64_t idx = 0;
         uint32_t jodd = 0;
 #pragma unroll
-        for (int a = kMaxRank - 1; a >= 0; a--) {
-            if (a < g.rank) {
-                uint32_t q = fdiv(rem, cm.cnt[a]);
-                uint32_t j = rem - q * cm.cnt[a].d;
-                rem = q;
-                int64_t c = cm.start[a] + (int64_t)j * cm.step[a];
-                coord[i][a] = (int32_t)c;
-                id += c * g.estr[a];
-                jodd |= (j & 1u) << a;
+        for (int a = 0; a < kMaxRank; a++) {
+            coord[a] = st[a] + j[a] * sp[a];
+            if (a < rank) {
+                idx += coord[a] * estr[a];
+                jodd |= (uint32_t)(j[a] & 1) << a;
             }
         }
-        idx[i] = id;
-        pp[i] = &cm.pred;
-        if (MIXED && mem[i]) {
-            int64_t b = 0;
-            for (int a = 0; a < g.rank; a++) b += (int64_t)(coord[i][a] / g.block_size) * g.bstr[a];
-            const int tag = P.table[(int64_t)cm.level * g.nblk + b];
-            const TagInfo &ti = P.tags[cm.tag_off + P.slots[cm.slot_off + tag]];
-            const int sp = ti.split;
-            if (cm.kind == COMMIT_MIXED_A) {
-                mem[i] = sp < 0 || !((jodd >> sp) & 1u);
-                pp[i] = &ti.inter;
-            } else {
-                int key = __popc(cm.axes_present & jodd & ~(1u << (sp < 0 ? 31 : sp)));
-                mem[i] = sp >= 0 && ((jodd >> sp) & 1u) && key == cm.phase;
-                pp[i] = &ti.same;
-            }
-        }
-    }
-    // pass 2: stream positions of the members
-    int64_t ci[kItems];
-    if (MIXED) {
-        uint32_t r[kItems], tot;
-        block_rank(mem, r, tot, s_rank);
-        const int64_t base = P.blkoff[ticket];
-#pragma unroll
-        for (int i = 0; i < kItems; i++) ci[i] = base + r[i];
-    } else {
-#pragma unroll
-        for (int i = 0; i < kItems; i++)
-            ci[i] = cm.code_base + (int64_t)(p0 + (uint32_t)(i * kThreads) + threadIdx.x);
-    }
-    // pass 3: predict + quantize / dequantize
-    bool esc[kItems];
-    double val[kItems];
-#pragma unroll
-    for (int i = 0; i < kItems; i++) {
-        esc[i] = false;
-        val[i] = 0.0;
-        if (!mem[i]) continue;
-        if (DIR == HPEZ_COMPRESS) {
-            const double pred = predict(g, work, idx[i], coord[i], *pp[i], cm.s);
-            const double orig = (double)work[idx[i]];
-            double out;
-            const int64_t code = quantize_point<ROUND>(orig, pred, cm.bound, cm.two_e, R, &out);
-            codes[ci[i]] = (C)code;
-            esc[i] = code == 0;
-            val[i] = orig;
-            if (STATS) {
-                const double err = fabs(__dsub_rn(orig, pred));
-                P.errbuf[ci[i]] = err;
-                if (P.dense) P.dense[(int64_t)cm.level * g.npts + idx[i]] = err;
-            }
-            if (!esc[i]) work[idx[i]] = (T)out;
-        } else {
-            const int64_t code = load_code(codes, ci[i]);
-            if (code == 0) {
-                esc[i] = true;
-            } else {
-                const double pred = predict(g, work, idx[i], coord[i], *pp[i], cm.s);
-                work[idx[i]] = (T)dequantize_point<ROUND>(pred, code, cm.two_e, R);
-            }
-        }
-    }
-    // pass 4: escapes in stream order (outliers)
-    uint32_t er[kItems], etot;
-    block_rank(esc, er, etot, s_rank);
-    if (threadIdx.x < 32) {
-        uint64_t ex = lookback(P.status, ticket, etot);
-        if (threadIdx.x == 0) s_excl = ex;
-    }
-    __syncthreads();
-    const int64_t ex = (int64_t)s_excl;
-#pragma unroll
-    for (int i = 0; i < kItems; i++) {
-        if (!esc[i]) continue;
-        const int64_t o = ex + er[i];
-        if (DIR == HPEZ_COMPRESS) {
-            if (o < P.outl_cap) P.outl[o] = val[i];
-        } else {
-            if (o < P.outl_cap) work[idx[i]] = (T)P.outl[o];
-            else atomicExch(P.flags, HPEZ_OUTLIER_UNDERFLOW);
-        }
-    }
-}
-
-// Data-independent member counts of mixed commits (one CTA per block).
-__global__ void __launch_bounds__(kThreads) mixed_count_kernel(const GridDev g, const CommitDev cm,
-                                                               const uint8_t *table,
-                                                               const TagInfo *tags,
-                                                               const uint8_t *slots,
-                                                               int64_t *blkcnt) {
-    __shared__ uint32_t s_rank[kItems * kWarps + 1];
-    const uint32_t p0 = blockIdx.x * (uint32_t)kBlockPos;
-    bool mem[kItems];
-#pragma unroll
-    for (int i = 0; i < kItems; i++) {
-        const uint32_t pos = p0 + (uint32_t)(i * kThreads) + threadIdx.x;
-        mem[i] = pos < cm.npos;
-        if (!mem[i]) continue;
-        uint32_t rem = pos, jodd = 0;
-        int64_t b = 0;
-        int32_t coord[kMaxRank];
-        for (int a = g.rank - 1; a >= 0; a--) {
-            uint32_t q = fdiv(rem, cm.cnt[a]);
-            uint32_t j = rem - q * cm.cnt[a].d;
-            rem = q;
-            coord[a] = (int32_t)(cm.start[a] + (int64_t)j * cm.step[a]);
-            jodd |= (j & 1u) << a;
-        }
-        for (int a = 0; a < g.rank; a++) b += (int64_t)(coord[a] / g.block_size) * g.bstr[a];
-        const int tag = table[(int64_t)cm.level * g.nblk + b];
-        const int sp = tags[cm.tag_off + slots[cm.slot_off + tag]].split;
-        if (cm.kind == COMMIT_MIXED_A) {
-            mem[i] = sp < 0 || !((jodd >> sp) & 1u);
-        } else {
-            int key = __popc(cm.axes_present & jodd & ~(1u << (sp < 0 ? 31 : sp)));
-            mem[i] = sp >= 0 && ((jodd >> sp) & 1u) && key == cm.phase;
-        }
-    }
-    uint32_t r[kItems], tot;
-    block_rank(mem, r, tot, s_rank);
-    if (threadIdx.x == 0) blkcnt[cm.blk_base + blockIdx.x] = tot;
-}
-
-// Exclusive scan of block counts over the commits of each mixed class, in
-// commit order (A, B_0, B_1, ...).  One CTA per class.
-struct ClassScan {
-    int64_t class_base;
-    int32_t c0, c1;  // commit index range
-};
-
-__global__ void __launch_bounds__(1024) mixed_scan_kernel(const ClassScan *cls,
-                                                          const int64_t *commit_blk_base,
-                                                          const int64_t *commit_nblk,
-                                                          const int64_t *blkcnt, int64_t *blkoff,
-                                                          int64_t *commit_code_base,
-                                                          int64_t *commit_n) {
-    __shared__ int64_t s_w[32];
-    __shared__ int64_t s_carry;
-    const ClassScan c = cls[blockIdx.x];
-    if (threadIdx.x == 0) s_carry = c.class_base;
-    __syncthreads();
-    for (int k = c.c0; k < c.c1; k++) {
-        const int64_t b0 = commit_blk_base[k], nb = commit_nblk[k];
-        const int64_t start = s_carry;
-        for (int64_t off = 0; off < nb; off += blockDim.x) {
-            const int64_t i = off + threadIdx.x;
-            int64_t v = i < nb ? blkcnt[b0 + i] : 0;
-            // block inclusive scan
-            int64_t x = v;
-            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-            for (int o = 1; o < 32; o <<= 1) {
-                int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            if (lane == 31) s_w[warp] = x;
-            __syncthreads();
-            if (warp == 0) {
-                int64_t w = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0;
-                for (int o = 1; o < 32; o <<= 1) {
-                    int64_t y = __shfl_up_sync(0xffffffffu, w, o);
-                    if (lane >= o) w += y;
+        bool member = valid;
+        PredReg pr = upred;
+        if (mixed && valid) pr = load_pred(*mixed_member(A, cmS, coord, jodd, &member));
+        const uint32_t mb = __ballot_sync(0xffffffffu, member);
+        const int64_t ci = cbase + __popc(mb & ((1u << lane) - 1u));
+        bool esc = false;
+        if (member) {
+            if (DIR == HPEZ_COMPRESS) {
+                const double pred = predict(work, idx, coord, dims, estr, pr, s);
+                const double orig = ldv(work, idx);
+                double out;
+                const int64_t code = quantize_point<ROUND>(orig, pred, bound, two_e, inv_two_e, R, &out);
+                __stcg(codes + ci, (C)code);
+                esc = code == 0;
+                if (!esc) __stcg(work + idx, (T)out);
+                if (STATS) {
+                    const double err = fabs(__dsub_rn(orig, pred));
+                    A.errbuf[ci] = err;
+                    if (A.dense) A.dense[(int64_t)cmS.level * A.g.npts + idx] = err;
                 }
-                s_w[lane] = w;
+            } else {
+                const int64_t code = (int64_t)codes[ci];
+                if (code != 0) {
+                    const double pred = predict(work, idx, coord, dims, estr, pr, s);
+                    __stcg(work + idx, (T)dequantize_point<ROUND>(pred, code, two_e, R));
+                } else {
+                    esc = true;
+                }
             }
-            __syncthreads();
-            const int64_t wpre = warp ? s_w[warp - 1] : 0;
-            const int64_t carry = s_carry;
-            if (i < nb) blkoff[b0 + i] = carry + wpre + x - v;
-            __syncthreads();
-            if (threadIdx.x == blockDim.x - 1) s_carry = carry + wpre + x;
-            __syncthreads();
         }
-        if (threadIdx.x == 0) {
-            commit_code_base[k] = start;
-            commit_n[k] = s_carry - start;
+        const uint32_t eb = __ballot_sync(0xffffffffu, esc);
+        if (DIR == HPEZ_DECOMPRESS && esc) {
+            const int64_t o = obase + nesc + __popc(eb & ((1u << lane) - 1u));
+            if (o < A.outl_cap) __stcg(work + idx, (T)A.outl[o]);
+            else atomicExch(A.flags, HPEZ_OUTLIER_UNDERFLOW);
+        }
+        nesc += __popc(eb);
+        cbase += __popc(mb);
+        // advance the lattice indices by 32 positions
+        if (inc) {
+            const int x = rank - 1;
+            int jx = pick(j, x) + 32;
+            bool carry = jx >= pick(cn, x);
+            if (carry) jx -= pick(cn, x);
+#pragma unroll
+            for (int a = kMaxRank - 1; a >= 0; a--) {
+                if (a == x) j[a] = jx;
+                else if (a < x && carry) {
+                    j[a] += 1;
+                    carry = j[a] >= cn[a];
+                    if (carry) j[a] = 0;
+                }
+            }
+        } else {
+            decode_pos(cmS, rank, p + 32, j);
+        }
+    }
+    if (DIR == HPEZ_COMPRESS && lane == 0) A.esc_cnt[e] = nesc;
+}
+
+// ------------------------------------------------- rank-3 fast paths --
+// Uniform commits of 3-D grids (every benchmark configuration) run through
+// one specialisation per (predictor layout, stencil family): KIND 0..2 = 1-D
+// along axis 0/1/2, 3..5 = MD blend over axes (0,1) (0,2) (1,2), 6 = MD over
+// (0,1,2).  Geometry is held in registers and lattice indices advance
+// incrementally, so the per-point cost is the stencil, the quantizer and a
+// few integer operations.
+template <int FAM, typename T>
+__device__ __forceinline__ double p1d(const T *__restrict__ w, int idx, int c, int E, int s, int sE) {
+    if (FAM == FAM_LIN_I) {
+        if (c + s <= E - 1) return DA(DM(0.5, ldv(w, idx - sE)), DM(0.5, ldv(w, idx + sE)));
+        return DM(1.0, ldv(w, idx - sE));
+    }
+    if (FAM == FAM_NAK_I || FAM == FAM_NAT_I) {
+        if (c >= 3 * s && c + 3 * s <= E - 1) {
+            const double a = ldv(w, idx - 3 * sE), b = ldv(w, idx - sE), d = ldv(w, idx + sE), e = ldv(w, idx + 3 * sE);
+            if (FAM == FAM_NAK_I)
+                return DA(DA(DA(DM(-1.0 / 16, a), DM(9.0 / 16, b)), DM(9.0 / 16, d)), DM(-1.0 / 16, e));
+            return DA(DA(DA(DM(-3.0 / 40, a), DM(23.0 / 40, b)), DM(23.0 / 40, d)), DM(-3.0 / 40, e));
+        }
+    } else if (FAM == FAM_NAK_S) {
+        if (c + 2 * s <= E - 1) {
+            const double a = ldv(w, idx - 2 * sE), b = ldv(w, idx - sE), d = ldv(w, idx + sE), e = ldv(w, idx + 2 * sE);
+            return DA(DA(DA(DM(-1.0 / 6, a), DM(4.0 / 6, b)), DM(4.0 / 6, d)), DM(-1.0 / 6, e));
+        }
+    } else {
+        if (c + 3 * s <= E - 1) {
+            const double a = ldv(w, idx - 3 * sE), b = ldv(w, idx - 2 * sE), d = ldv(w, idx - sE),
+                         e = ldv(w, idx + sE), f = ldv(w, idx + 2 * sE), h = ldv(w, idx + 3 * sE);
+            return DA(DA(DA(DA(DA(DM(3.0 / 62, a), DM(-18.0 / 62, b)), DM(46.0 / 62, d)), DM(46.0 / 62, e)),
+                         DM(-18.0 / 62, f)), DM(3.0 / 62, h));
+        }
+    }
+    return pred_table(w, (int64_t)idx, c, E, s, (int64_t)sE, FAM);
+}
+
+template <typename T, typename C, int DIR, int ROUND, int KIND, int FAM>
+__device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev &cm, int item, int warp) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t p0 = (uint32_t)(item - cm.item_base) * (uint32_t)cm.p_item + (uint32_t)warp * (uint32_t)cm.pw;
+    const uint32_t pend = min(p0 + (uint32_t)cm.pw, cm.npos);
+    const int e = item * kItemWarps + warp;
+    if (p0 >= pend) {
+        if (DIR == HPEZ_COMPRESS && lane == 0) A.esc_cnt[e] = 0;
+        return;
+    }
+    const int st0 = cm.start[0], st1 = cm.start[1], st2 = cm.start[2];
+    const int sp0 = cm.step[0], sp1 = cm.step[1], sp2 = cm.step[2];
+    const int cn1 = cm.cnt[1], cn2 = cm.cnt[2];
+    const int D0 = A.g.dims[0], D1 = A.g.dims[1], D2 = A.g.dims[2];
+    const int E0 = A.g.estr[0], E1 = A.g.estr[1];
+    const int s = cm.s;
+    const int sE0 = s * E0, sE1 = s * E1, sE2 = s;
+    const double bound = cm.bound, two_e = cm.two_e, inv_two_e = cm.inv_two_e;
+    const double w0 = cm.pred.w[0], w1 = cm.pred.w[1], w2 = cm.pred.w[2];
+    const int64_t R = A.g.radius;
+    T *__restrict__ work = (T *)A.work;
+    C *__restrict__ codes = (C *)A.codes;
+    const int64_t cb = cm.code_base;
+    const int64_t obase = DIR == HPEZ_DECOMPRESS ? A.esc_off[e] : 0;
+    uint32_t nesc = 0;
+    uint32_t p = p0 + lane;
+    uint32_t r = fdiv(p, cm.fd[2]);
+    int jx = (int)(p - r * (uint32_t)cn2);
+    uint32_t q = fdiv(r, cm.fd[1]);
+    int jy = (int)(r - q * (uint32_t)cn1);
+    int jz = (int)q;
+    for (uint32_t pb = p0; pb < pend; pb += 32) {
+        const bool valid = pb + lane < pend;
+        const int z = st0 + jz * sp0, y = st1 + jy * sp1, x = st2 + jx * sp2;
+        const int idx = z * E0 + y * E1 + x;
+        const int64_t ci = cb + pb + lane;
+        bool esc = false;
+        if (valid) {
+            auto predict_fast = [&]() -> double {
+                if (KIND == 0) return p1d<FAM>(work, idx, z, D0, s, sE0);
+                if (KIND == 1) return p1d<FAM>(work, idx, y, D1, s, sE1);
+                if (KIND == 2) return p1d<FAM>(work, idx, x, D2, s, sE2);
+                if (KIND == 3) return DA(DM(w0, p1d<FAM>(work, idx, z, D0, s, sE0)), DM(w1, p1d<FAM>(work, idx, y, D1, s, sE1)));
+                if (KIND == 4) return DA(DM(w0, p1d<FAM>(work, idx, z, D0, s, sE0)), DM(w1, p1d<FAM>(work, idx, x, D2, s, sE2)));
+                if (KIND == 5) return DA(DM(w0, p1d<FAM>(work, idx, y, D1, s, sE1)), DM(w1, p1d<FAM>(work, idx, x, D2, s, sE2)));
+                return DA(DA(DM(w0, p1d<FAM>(work, idx, z, D0, s, sE0)), DM(w1, p1d<FAM>(work, idx, y, D1, s, sE1))),
+                          DM(w2, p1d<FAM>(work, idx, x, D2, s, sE2)));
+            };
+            if (DIR == HPEZ_COMPRESS) {
+                const double pred = predict_fast();
+                const double orig = ldv(work, idx);
+                double out;
+                const int64_t code = quantize_point<ROUND>(orig, pred, bound, two_e, inv_two_e, R, &out);
+                __stcg(codes + ci, (C)code);
+                esc = code == 0;
+                if (!esc) __stcg(work + idx, (T)out);
+            } else {
+                const int64_t code = (int64_t)codes[ci];
+                if (code != 0) {
+                    const double pred = predict_fast();
+                    __stcg(work + idx, (T)dequantize_point<ROUND>(pred, code, two_e, R));
+                } else {
+                    esc = true;
+                }
+            }
+        }
+        const uint32_t eb = __ballot_sync(0xffffffffu, esc);
+        if (DIR == HPEZ_DECOMPRESS && esc) {
+            const int64_t o = obase + nesc + __popc(eb & ((1u << lane) - 1u));
+            if (o < A.outl_cap) __stcg(work + idx, (T)A.outl[o]);
+            else atomicExch(A.flags, HPEZ_OUTLIER_UNDERFLOW);
+        }
+        nesc += __popc(eb);
+        jx += 32;
+        while (jx >= cn2) {
+            jx -= cn2;
+            if (++jy >= cn1) {
+                jy = 0;
+                jz++;
+            }
+        }
+    }
+    if (DIR == HPEZ_COMPRESS && lane == 0) A.esc_cnt[e] = nesc;
+}
+
+// fast_id = KIND * 5 + FAM (MD kinds use inter families 0..2 only)
+template <typename T, typename C, int DIR, int ROUND>
+__device__ __forceinline__ void process_dispatch(const SweepArgs &A, const CommitDev &cm, int item, int warp) {
+#define HPEZ_FAST(K, F)                                                  \
+    case K * 5 + F:                                                      \
+        process_fast<T, C, DIR, ROUND, K, F>(A, cm, item, warp);         \
+        return;
+    switch (cm.fast_id) {
+        HPEZ_FAST(0, 0) HPEZ_FAST(0, 1) HPEZ_FAST(0, 2) HPEZ_FAST(0, 3) HPEZ_FAST(0, 4)
+        HPEZ_FAST(1, 0) HPEZ_FAST(1, 1) HPEZ_FAST(1, 2) HPEZ_FAST(1, 3) HPEZ_FAST(1, 4)
+        HPEZ_FAST(2, 0) HPEZ_FAST(2, 1) HPEZ_FAST(2, 2) HPEZ_FAST(2, 3) HPEZ_FAST(2, 4)
+        HPEZ_FAST(3, 0) HPEZ_FAST(3, 1) HPEZ_FAST(3, 2)
+        HPEZ_FAST(4, 0) HPEZ_FAST(4, 1) HPEZ_FAST(4, 2)
+        HPEZ_FAST(5, 0) HPEZ_FAST(5, 1) HPEZ_FAST(5, 2)
+        HPEZ_FAST(6, 0) HPEZ_FAST(6, 1) HPEZ_FAST(6, 2)
+    default:
+        break;
+    }
+#undef HPEZ_FAST
+}
+
+// Leading tiny levels: one CTA of 4 groups x 8 warps.  All commits of one
+// (level, DAG depth) group are independent and run concurrently; groups are
+// separated by __syncthreads.
+__device__ __forceinline__ void group_bar(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kItemThreads) : "memory");
+}
+
+template <typename T, typename C, int DIR, int ROUND, bool STATS, bool FAST>
+__global__ void __launch_bounds__(1024) coarse_kernel(const __grid_constant__ SweepArgs A) {
+    __shared__ CommitDev s_cm[4];
+    const int group = threadIdx.x / kItemThreads;
+    const int gt = threadIdx.x % kItemThreads;
+    const int warp = gt >> 5;
+    for (int g = 0; g < A.n_groups; g++) {
+        const int t0 = A.coarse_groups[2 * g], t1 = A.coarse_groups[2 * g + 1];
+        for (int t = t0 + group; t < t1; t += 4) {
+            const int c = A.coarse_pairs[2 * t], item = A.coarse_pairs[2 * t + 1];
+            if (gt < sizeof(CommitDev) / 4)
+                ((uint32_t *)&s_cm[group])[gt] = ((const uint32_t *)&A.commits[c])[gt];
+            group_bar(group + 1);
+            if (FAST) process_dispatch<T, C, DIR, ROUND>(A, s_cm[group], item, warp);
+            else process_warp<T, C, DIR, ROUND, STATS>(A, s_cm[group], item, warp);
+            group_bar(group + 1);
         }
         __syncthreads();
     }
 }
 
-// numpy pairwise sum (loops_utils.h pairwise_sum) of each commit's member
-// errors, leaves in parallel, tree folded by one thread in recursion order.
+// Persistent dataflow kernel over the remaining items.
+template <typename T, typename C, int DIR, int ROUND, bool STATS, bool FAST>
+__global__ void __launch_bounds__(kItemThreads, FAST ? 4 : 3) flow_kernel(const __grid_constant__ SweepArgs A) {
+    __shared__ CommitDev s_cm;
+    __shared__ int s_item;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int cur = -1;
+    while (true) {
+        if (threadIdx.x == 0) s_item = atomicAdd(A.next, 1);
+        __syncthreads();
+        const int rel = s_item;
+        if (rel >= A.n_items) break;
+        const int item = A.flow_order[rel];
+        const int c = A.item_commit[item];
+        if (c != cur) {
+            if (threadIdx.x < sizeof(CommitDev) / 4)
+                ((uint32_t *)&s_cm)[threadIdx.x] = ((const uint32_t *)&A.commits[c])[threadIdx.x];
+            cur = c;
+        }
+        if (warp == 0) {
+            const int k0 = A.dep_off[item], k1 = A.dep_off[item + 1];
+            for (int k = k0; k < k1; k++) {
+                const int2 d = A.dep_rng[k];
+                for (int q = d.x + lane; q <= d.y; q += 32)
+                    while (ld_relaxed(&A.done[q]) == 0) __nanosleep(32);
+            }
+            __threadfence();
+        }
+        __syncthreads();
+        if (FAST) process_dispatch<T, C, DIR, ROUND>(A, s_cm, item, warp);
+        else process_warp<T, C, DIR, ROUND, STATS>(A, s_cm, item, warp);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release(&A.done[item], 1u);
+    }
+}
+
+// Decompress pre-pass: zero codes per (item, warp).
+template <typename C>
+__global__ void __launch_bounds__(256) count_zero_kernel(const C *__restrict__ codes, const int64_t *__restrict__ wbase,
+                                                         const int32_t *__restrict__ wn, int64_t n_entries,
+                                                         uint32_t *__restrict__ cnt) {
+    const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (e >= n_entries) return;
+    const int64_t b = wbase[e];
+    const int n = wn[e];
+    uint32_t z = 0;
+    for (int i = lane; i < n; i += 32) z += codes[b + i] == 0;
+    for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    if (lane == 0) cnt[e] = z;
+}
+
+// Compress post-pass: outliers of every (item, warp) with escapes, in stream
+// order, read back from the grid (escaped points keep their originals).
+template <typename T, typename C>
+__global__ void __launch_bounds__(256) gather_outliers_kernel(const __grid_constant__ SweepArgs A, int64_t n_entries,
+                                                              double *__restrict__ out, int64_t cap) {
+    const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (e >= n_entries || A.esc_cnt[e] == 0) return;
+    const int item = (int)(e / kItemWarps), warp = (int)(e % kItemWarps);
+    const CommitDev &cm = A.commits[A.item_commit[item]];
+    const GridDev &g = A.g;
+    const T *work = (const T *)A.work;
+    const C *codes = (const C *)A.codes;
+    const uint32_t p0 = (uint32_t)(item - cm.item_base) * (uint32_t)cm.p_item + (uint32_t)warp * (uint32_t)cm.pw;
+    const uint32_t pend = min(p0 + (uint32_t)cm.pw, cm.npos);
+    int64_t cbase = A.wbase[e];
+    int64_t o = A.esc_off[e];
+    if (cm.kind == COMMIT_UNIFORM) {
+        // members are all positions: scan the warp's code range for escapes
+        const int n = (int)(pend - p0);
+        for (int k = 0; k < n; k += 32) {
+            const bool esc = k + lane < n && codes[cbase + k + lane] == 0;
+            const uint32_t eb = __ballot_sync(0xffffffffu, esc);
+            if (esc) {
+                int j[kMaxRank];
+                decode_pos(cm, g.rank, p0 + k + lane, j);
+                int64_t idx = 0;
+                for (int a = 0; a < g.rank; a++) idx += (int64_t)(cm.start[a] + j[a] * cm.step[a]) * g.estr[a];
+                const int64_t r = o + __popc(eb & ((1u << lane) - 1u));
+                if (r < cap) out[r] = (double)work[idx];
+            }
+            o += __popc(eb);
+        }
+        return;
+    }
+    for (uint32_t pb = p0; pb < pend; pb += 32) {
+        const uint32_t p = pb + lane;
+        const bool valid = p < pend;
+        int j[kMaxRank], coord[kMaxRank];
+        decode_pos(cm, g.rank, valid ? p : p0, j);
+        int64_t idx = 0;
+        uint32_t jodd = 0;
+        for (int a = 0; a < g.rank; a++) {
+            coord[a] = cm.start[a] + j[a] * cm.step[a];
+            idx += (int64_t)coord[a] * g.estr[a];
+            jodd |= (uint32_t)(j[a] & 1) << a;
+        }
+        bool member = valid;
+        if (valid) mixed_member(A, cm, coord, jodd, &member);
+        const uint32_t mb = __ballot_sync(0xffffffffu, member);
+        const int64_t ci = cbase + __popc(mb & ((1u << lane) - 1u));
+        const bool esc = member && codes[ci] == 0;
+        const uint32_t eb = __ballot_sync(0xffffffffu, esc);
+        if (esc) {
+            const int64_t r = o + __popc(eb & ((1u << lane) - 1u));
+            if (r < cap) out[r] = (double)work[idx];
+        }
+        o += __popc(eb);
+        cbase += __popc(mb);
+    }
+}
+
+// Mixed setup: member counts per (item, warp) of mixed commits.
+__global__ void __launch_bounds__(256) mixed_count_kernel(const __grid_constant__ SweepArgs A, int32_t *wn_out,
+                                                          int32_t n_mixed_items, const int32_t *mixed_items) {
+    const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= (int64_t)n_mixed_items * kItemWarps) return;
+    const int item = mixed_items[t / kItemWarps], warp = (int)(t % kItemWarps);
+    const CommitDev &cm = A.commits[A.item_commit[item]];
+    const GridDev &g = A.g;
+    const uint32_t p0 = (uint32_t)(item - cm.item_base) * (uint32_t)cm.p_item + (uint32_t)warp * (uint32_t)cm.pw;
+    const uint32_t pend = min(p0 + (uint32_t)cm.pw, cm.npos);
+    int n = 0;
+    for (uint32_t pb = p0; pb < pend; pb += 32) {
+        const uint32_t p = pb + lane;
+        bool member = false;
+        if (p < pend) {
+            int j[kMaxRank], coord[kMaxRank];
+            decode_pos(cm, g.rank, p, j);
+            uint32_t jodd = 0;
+            for (int a = 0; a < g.rank; a++) {
+                coord[a] = cm.start[a] + j[a] * cm.step[a];
+                jodd |= (uint32_t)(j[a] & 1) << a;
+            }
+            mixed_member(A, cm, coord, jodd, &member);
+        }
+        n += __popc(__ballot_sync(0xffffffffu, member));
+    }
+    if (lane == 0) wn_out[(int64_t)item * kItemWarps + warp] = n;
+}
+
+// ------------------------------------------------------- exclusive scan --
+// Three-phase exclusive scan of n counts into i64 offsets.
+constexpr int kScanBlock = 1024;
+constexpr int kScanPer = 4;
+constexpr int kScanTile = kScanBlock * kScanPer;
+
+template <typename V>
+__global__ void __launch_bounds__(kScanBlock) scan_tiles_kernel(const V *__restrict__ in, int64_t n,
+                                                                int64_t *__restrict__ out,
+                                                                int64_t *__restrict__ tile_sum) {
+    __shared__ int64_t s_w[32];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanPer;
+    int64_t v[kScanPer], t = 0;
+    for (int k = 0; k < kScanPer; k++) {
+        v[k] = base + k < n ? (int64_t)in[base + k] : 0;
+        t += v[k];
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t x = t;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int64_t w = s_w[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        s_w[lane] = w;
+    }
+    __syncthreads();
+    int64_t run = (warp ? s_w[warp - 1] : 0) + x - t;
+    for (int k = 0; k < kScanPer; k++) {
+        if (base + k < n) out[base + k] = run;
+        run += v[k];
+    }
+    if (threadIdx.x == kScanBlock - 1) tile_sum[blockIdx.x] = run;
+}
+
+__global__ void __launch_bounds__(1024) scan_sums_kernel(int64_t *sums, int64_t n, int64_t *total) {
+    __shared__ int64_t s_w[32];
+    __shared__ int64_t s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t off = 0; off < n; off += blockDim.x) {
+        const int64_t i = off + threadIdx.x;
+        const int64_t x0 = i < n ? sums[i] : 0;
+        int64_t x = x0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int64_t w = s_w[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            s_w[lane] = w;
+        }
+        __syncthreads();
+        const int64_t carry = s_carry;
+        const int64_t pre = (warp ? s_w[warp - 1] : 0) + x - x0;
+        if (i < n) sums[i] = carry + pre;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_carry = carry + pre + x0;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && total) *total = s_carry;
+}
+
+__global__ void scan_add_kernel(int64_t *__restrict__ out, int64_t n, const int64_t *__restrict__ tile_off) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] += tile_off[i / kScanTile];
+}
+
+template <typename V>
+static void exclusive_scan(const V *in, int64_t n, int64_t *out, int64_t *tmp, int64_t *total, cudaStream_t st) {
+    if (n == 0) {
+        cudaMemsetAsync(total, 0, sizeof(int64_t), st);
+        return;
+    }
+    const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+    scan_tiles_kernel<V><<<(unsigned)tiles, kScanBlock, 0, st>>>(in, n, out, tmp);
+    scan_sums_kernel<<<1, 1024, 0, st>>>(tmp, tiles, total);
+    scan_add_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(out, n, tmp);
+}
+
+// ---------------------------------------------------- stats (tuning) --
 __device__ double leaf_sum(const double *a, int64_t n) {
     if (n < 8) {
         double r = -0.0;
@@ -422,92 +843,75 @@ __device__ double leaf_sum(const double *a, int64_t n) {
     return res;
 }
 
+// numpy pairwise sum of each commit's member errors (numpy order).
 __global__ void commit_pairwise_kernel(const double *errbuf, const int64_t *commit_code_base,
-                                       const int64_t *commit_n, double *commit_sum,
-                                       double *leafbuf, const int64_t *leaf_off) {
+                                       const int64_t *commit_n, double *commit_sum) {
     const int c = blockIdx.x;
     const int64_t base = commit_code_base[c], n = commit_n[c];
-    double *leaves = leafbuf + leaf_off[c];
-    // Leaves left to right (pairwise splits until n <= 128), then the fold in
-    // the same recursion order.  Trial commits are small (<= ~35K members).
+    if (threadIdx.x != 0) return;
     if (n == 0) {
-        if (threadIdx.x == 0) commit_sum[c] = 0.0;
+        commit_sum[c] = 0.0;
         return;
     }
-    int64_t leaf = 0;
-    if (threadIdx.x == 0) {
-        int64_t ls[64], ln[64];
-        int top = 0;
-        ls[0] = 0;
-        ln[0] = n;
-        top = 1;
-        while (top) {
+    double vs[64];
+    int64_t fs[64], fn[64];
+    int32_t state[64];
+    int vt = 0, top = 1;
+    fs[0] = 0;
+    fn[0] = n;
+    state[0] = 0;
+    while (top) {
+        const int t = top - 1;
+        if (fn[t] <= 128) {
+            vs[vt++] = leaf_sum(errbuf + base + fs[t], fn[t]);
             top--;
-            const int64_t s0 = ls[top], n0 = ln[top];
-            if (n0 <= 128) {
-                leaves[leaf++] = leaf_sum(errbuf + base + s0, n0);
-                continue;
-            }
-            int64_t n2 = n0 / 2;
-            n2 -= n2 % 8;
-            ls[top] = s0 + n2;  // right child visited second
-            ln[top] = n0 - n2;
-            top++;
-            ls[top] = s0;
-            ln[top] = n2;
-            top++;
+            continue;
         }
-        // fold in the same recursion order
-        double vs[64];
-        int64_t fs[64], fn[64];
-        int32_t state[64];
-        int vt = 0;
-        top = 0;
-        fs[0] = 0;
-        fn[0] = n;
-        state[0] = 0;
-        top = 1;
-        int64_t li = 0;
-        while (top) {
-            const int t = top - 1;
-            if (fn[t] <= 128) {
-                vs[vt++] = leaves[li++];
-                top--;
-                continue;
-            }
-            int64_t n2 = fn[t] / 2;
-            n2 -= n2 % 8;
-            if (state[t] == 0) {
-                state[t] = 1;
-                fs[top] = fs[t];
-                fn[top] = n2;
-                state[top] = 0;
-                top++;
-            } else if (state[t] == 1) {
-                state[t] = 2;
-                fs[top] = fs[t] + n2;
-                fn[top] = fn[t] - n2;
-                state[top] = 0;
-                top++;
-            } else {
-                const double b = vs[--vt], a = vs[--vt];
-                vs[vt++] = __dadd_rn(a, b);
-                top--;
-            }
+        int64_t n2 = fn[t] / 2;
+        n2 -= n2 % 8;
+        if (state[t] == 0) {
+            state[t] = 1;
+            fs[top] = fs[t];
+            fn[top] = n2;
+            state[top] = 0;
+            top++;
+        } else if (state[t] == 1) {
+            state[t] = 2;
+            fs[top] = fs[t] + n2;
+            fn[top] = fn[t] - n2;
+            state[top] = 0;
+            top++;
+        } else {
+            const double b = vs[--vt], a = vs[--vt];
+            vs[vt++] = __dadd_rn(a, b);
+            top--;
         }
-        commit_sum[c] = vs[0];
     }
+    commit_sum[c] = vs[0];
 }
 
-__global__ void stats_accumulate_kernel(int n_commits, const int32_t *commit_level,
-                                        const double *commit_sum, const int64_t *commit_n,
-                                        double *err_sum, int64_t *count) {
+__global__ void stats_accumulate_kernel(int n_commits, const int32_t *commit_level, const double *commit_sum,
+                                        const int64_t *commit_n, double *err_sum, int64_t *count) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     for (int c = 0; c < n_commits; c++) {
         if (commit_n[c] == 0) continue;  // empty commits are never recorded
         err_sum[commit_level[c]] = __dadd_rn(err_sum[commit_level[c]], commit_sum[c]);
         count[commit_level[c]] += commit_n[c];
     }
+}
+
+// Per-commit code base and member count from the (item, warp) table.
+__global__ void commit_ranges_kernel(const CommitDev *commits, int nc, const int64_t *wbase, const int32_t *wn,
+                                     int64_t *cbase, int64_t *cn) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const CommitDev &cm = commits[c];
+    const int64_t e0 = (int64_t)cm.item_base * kItemWarps;
+    const int64_t e1 = (int64_t)(cm.item_base + cm.n_items) * kItemWarps;
+    int64_t n = 0;
+    for (int64_t e = e0; e < e1; e++) n += wn[e];
+    cbase[c] = wbase[e0];
+    cn[c] = n;
 }
 
 // ----------------------------------------------------------- host plan --
@@ -537,6 +941,19 @@ static double py_sum(const std::vector<double> &x) {
     return r;
 }
 
+static int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+constexpr uint32_t kCoarseMax = 4096;  // commits at most this large run in the coarse CTA
+
 struct Plan {
     hpez_sweep_desc d{};
     std::vector<hpez_level> levels;
@@ -549,40 +966,57 @@ struct Plan {
     std::vector<CommitDev> commits;
     std::vector<TagInfo> tags;
     std::vector<uint8_t> slots;
-    std::vector<ClassScan> classes;
     bool has_mixed = false;
-    int64_t total_blocks = 0;
     int64_t num_codes = 0;
-    int64_t leaf_total = 0;
     std::vector<int64_t> level_codes;
+    int32_t n_items = 0;
+    int32_t c_coarse = 0;      // commits [0, c_coarse) run in the coarse kernel
+    bool coarse_fast = false, flow_fast = false;
+    int32_t first_flow_item = 0;
+    std::vector<int32_t> item_commit;
+    std::vector<int32_t> dep_off;     // per item: first entry in dep_rng
+    std::vector<int2> dep_rng;        // item-id intervals an item waits on
+    std::vector<int32_t> flow_order;  // flow items in grab order
+    std::vector<int32_t> coarse_pairs;   // coarse (commit, item) pairs, depth-grouped
+    std::vector<int32_t> coarse_groups;  // boundaries into coarse_pairs (pairs of ints)
+    std::vector<uint32_t> c_vmask, c_reads;
+    std::vector<int32_t> wn;   // member count per (item, warp); mixed filled on device
+    std::vector<int32_t> mixed_items;
 
     // device
-    uint64_t *d_status = nullptr;
-    unsigned long long *d_counters = nullptr;  // [0] ticket, [1] flags
-    int64_t *d_blkoff = nullptr;
-    int64_t *d_blkcnt = nullptr;
+    CommitDev *d_commits = nullptr;
+    int32_t *d_item_commit = nullptr;
+    int32_t *d_flow_order = nullptr, *d_dep_off = nullptr, *d_coarse_pairs = nullptr, *d_coarse_groups = nullptr;
+    int2 *d_dep_rng = nullptr;
+    int64_t *d_wbase = nullptr;
+    int32_t *d_wn = nullptr;
+    uint32_t *d_esc_cnt = nullptr;
+    int64_t *d_esc_off = nullptr;
+    int64_t *d_scan_tmp = nullptr;
+    int64_t *d_total = nullptr;   // [0] outlier total
+    uint32_t *d_done = nullptr;
+    int32_t *d_counters = nullptr;  // [0] next flow item, [1] flags
     TagInfo *d_tags = nullptr;
     uint8_t *d_slots = nullptr;
     uint8_t *d_table = nullptr;
-    ClassScan *d_classes = nullptr;
-    int64_t *d_cblk = nullptr, *d_cnblk = nullptr, *d_cbase = nullptr, *d_cn = nullptr;
+    int32_t *d_mixed_items = nullptr;
+    int64_t *d_cbase = nullptr, *d_cn = nullptr;
     int32_t *d_clevel = nullptr;
-    double *d_errbuf = nullptr, *d_csum = nullptr, *d_leaves = nullptr;
-    int64_t *d_leafoff = nullptr;
+    double *d_errbuf = nullptr, *d_csum = nullptr;
     bool setup_done = false;
     int64_t outl_cap_last = 0;
-    int direction = 0;
+    int flow_grid = 0;
 
     ~Plan() {
-        void *ptrs[] = {d_status, d_counters, d_blkoff, d_blkcnt, d_tags, d_slots, d_table,
-                        d_classes, d_cblk, d_cnblk, d_cbase, d_cn, d_clevel, d_errbuf,
-                        d_csum, d_leaves, d_leafoff};
+        void *ptrs[] = {d_commits, d_item_commit, d_flow_order, d_dep_off, d_coarse_pairs, d_coarse_groups,
+                        d_dep_rng, d_wbase, d_wn, d_esc_cnt, d_esc_off,
+                        d_scan_tmp, d_total, d_done, d_counters, d_tags, d_slots, d_table,
+                        d_mixed_items, d_cbase, d_cn, d_clevel, d_errbuf, d_csum};
         for (void *p : ptrs)
             if (p) cudaFree(p);
     }
 
-    // plan.order_candidates (plan.py:37-51)
-    std::vector<std::vector<int>> order_candidates() const {
+    std::vector<std::vector<int>> order_candidates() const {  // plan.py:37-51
         std::vector<std::vector<int>> out;
         std::vector<int> ax = active;
         if (ax.size() <= 3) {
@@ -663,18 +1097,20 @@ struct Plan {
         c.s = levels[li].stride;
         c.bound = levels[li].bound;
         c.two_e = 2.0 * levels[li].bound;
+        c.inv_two_e = c.two_e > 0.0 ? 1.0 / c.two_e : 0.0;
         int64_t npos = 1;
         for (int a = 0; a < d.rank; a++) {
-            c.start[a] = start[a];
-            c.step[a] = step[a];
-            c.cnt[a] = make_fastdiv((uint32_t)count[a]);
+            c.start[a] = (int32_t)start[a];
+            c.step[a] = (int32_t)step[a];
+            c.cnt[a] = (int32_t)count[a];
+            c.fd[a] = make_fastdiv((uint32_t)count[a]);
             npos *= count[a];
         }
-        for (int a = d.rank; a < kMaxRank; a++) c.cnt[a] = make_fastdiv(1);
+        for (int a = d.rank; a < kMaxRank; a++) {
+            c.cnt[a] = 1;
+            c.fd[a] = make_fastdiv(1);
+        }
         c.npos = (uint32_t)npos;
-        c.nblocks = (uint32_t)((npos + kBlockPos - 1) / kBlockPos);
-        c.blk_base = total_blocks;
-        total_blocks += c.nblocks;
         c.commit_id = (int)commits.size();
         return c;
     }
@@ -707,6 +1143,10 @@ struct Plan {
             cm.code_base = *code_pos;
             *code_pos += tot;
             commits.push_back(cm);
+            uint32_t vm = 0;
+            for (int a : v) vm |= 1u << a;
+            c_vmask.push_back(vm);
+            c_reads.push_back(cm.pred.md ? vm : (1u << cm.pred.axis));
         }
     }
 
@@ -720,12 +1160,12 @@ struct Plan {
         int64_t n = 1;
         for (int a = d.rank - 1; a >= 0; a--) {
             if (d.dims[a] < 1) return HPEZ_BAD_ARGUMENT;
-            g.dims[a] = d.dims[a];
-            g.estr[a] = n;
+            g.dims[a] = (int32_t)d.dims[a];
+            g.estr[a] = (int32_t)n;
             n *= d.dims[a];
+            if (n >= (1ll << 31)) return HPEZ_BAD_ARGUMENT;  // per-field limit of this build
         }
         g.npts = n;
-        if (n >= (1ll << 31)) return HPEZ_BAD_ARGUMENT;  // per-field limit of this build
         for (int a = 0; a < d.rank; a++)
             if (!(d.frozen_mask >> a & 1)) active.push_back(a);
         md.assign(d.rank, 1.0);  // interp.py:457-458
@@ -736,7 +1176,7 @@ struct Plan {
         if (use_tbl) {
             int64_t nb = 1;
             for (int a = d.rank - 1; a >= 0; a--) {
-                g.bstr[a] = nb;
+                g.bstr[a] = (int32_t)nb;
                 nb *= (d.dims[a] + d.block_size - 1) / d.block_size;
             }
             nblk_table = nb;
@@ -781,7 +1221,7 @@ struct Plan {
                         tot *= count[a];
                     }
                     if (tot > 0) {
-                        int st = use_tbl ? add_class_table(li, lc, v, start, step, count, tot, &code_pos)
+                        int st = use_tbl ? add_class_table(li, v, start, step, count, tot, &code_pos)
                                          : (add_uniform(li, lc, v, start, step, count, &code_pos), 0);
                         if (st) return st;
                     }
@@ -795,11 +1235,12 @@ struct Plan {
             level_codes.push_back(code_pos);
         }
         num_codes = code_pos;
+        build_items();
         return HPEZ_OK;
     }
 
-    int add_class_table(int li, const Cfg &, const std::vector<int> &v, const int64_t *start,
-                        const int64_t *step, const int64_t *count, int64_t tot, int64_t *code_pos) {
+    int add_class_table(int li, const std::vector<int> &v, const int64_t *start, const int64_t *step,
+                        const int64_t *count, int64_t tot, int64_t *code_pos) {
         // np.unique over the class lattice tags (interp.py:423-432): the set of
         // blocks hit per axis, then their product.
         std::vector<std::vector<int64_t>> hit(d.rank);
@@ -828,7 +1269,6 @@ struct Plan {
             add_uniform(li, c, v, start, step, count, code_pos);
             return 0;
         }
-        // mixed class
         has_mixed = true;
         const int tag_off = (int)tags.size();
         const int slot_off = (int)slots.size();
@@ -850,9 +1290,6 @@ struct Plan {
             tags.push_back(ti);
             slots[slot_off + t] = (uint8_t)slot++;
         }
-        ClassScan cs{};
-        cs.class_base = *code_pos;
-        cs.c0 = (int)commits.size();
         const int nph = __builtin_popcount(axes_present);
         for (int ph = -1; ph < nph; ph++) {
             CommitDev cm = base_commit(li, start, step, count);
@@ -863,12 +1300,188 @@ struct Plan {
             cm.slot_off = slot_off;
             cm.code_base = -1;
             commits.push_back(cm);
+            uint32_t vm = 0;
+            for (int a : v) vm |= 1u << a;
+            c_vmask.push_back(vm);
+            c_reads.push_back(vm);  // any tag may predict along any class axis
         }
-        cs.c1 = (int)commits.size();
-        classes.push_back(cs);
         *code_pos += tot;
         return 0;
     }
+
+    // Rank-3 uniform specialisation id (KIND * 5 + FAM) or -1.
+    int fast_id_of(const CommitDev &cm) const {
+        if (d.rank != 3 || cm.kind != COMMIT_UNIFORM || d.with_stats) return -1;
+        const PredDev &p = cm.pred;
+        if (!p.md) return p.axis * 5 + p.fam;
+        if (p.fam > FAM_NAT_I) return -1;
+        if (p.nax == 3) return 6 * 5 + p.fam;
+        if (p.nax != 2) return -1;
+        const int a = p.axes[0], b = p.axes[1];
+        const int kind = (a == 0 && b == 1) ? 3 : (a == 0 && b == 2) ? 4 : (a == 1 && b == 2) ? 5 : -1;
+        return kind < 0 ? -1 : kind * 5 + p.fam;
+    }
+
+    // Item interval of commit `pv` covering the outer-axis window of item
+    // `it` of commit `cm` (stencil reach +-3s, plus one plane of pv on each
+    // side so that coverage stays transitive along dependency chains).
+    int2 dep_interval(const CommitDev &cm, int it, const CommitDev &pv) const {
+        const int64_t U = (int64_t)cm.npos / cm.cnt[0];
+        const int64_t pa = (int64_t)it * cm.p_item;
+        const int64_t pb = std::min<int64_t>(pa + cm.p_item, cm.npos) - 1;
+        const int64_t zlo = cm.start[0] + (pa / U) * (int64_t)cm.step[0] - 3 * (int64_t)cm.s;
+        const int64_t zhi = cm.start[0] + (pb / U) * (int64_t)cm.step[0] + 3 * (int64_t)cm.s;
+        auto fl = [](int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+        int64_t ja = fl(zlo - pv.start[0], pv.step[0]);
+        int64_t jb = -fl(-(zhi - pv.start[0]), pv.step[0]);
+        ja = std::max<int64_t>(0, std::min<int64_t>(ja, pv.cnt[0] - 1));
+        jb = std::max<int64_t>(0, std::min<int64_t>(jb, pv.cnt[0] - 1));
+        const int64_t Up = (int64_t)pv.npos / pv.cnt[0];
+        const int64_t qa = ja * Up, qb = std::min<int64_t>((jb + 1) * Up, pv.npos) - 1;
+        return int2{pv.item_base + (int)(qa / pv.p_item), pv.item_base + (int)(qb / pv.p_item)};
+    }
+
+    // Work items, (item, warp) tables, the commit dependency DAG and the
+    // dependency intervals.  A commit of class v at level l reads (a) points
+    // of classes v \ {a} of level l for every axis a it predicts along,
+    // (b) earlier phases of its own class (same-level stencils, mixed B
+    // commits), (c) coarser points, all produced by ancestors of the sinks of
+    // the previous level's DAG.  Items are grabbed in (level, depth, outer
+    // coordinate) order, so independent commits run concurrently.
+    void build_items() {
+        const int sms = num_sms();
+        const int nc = (int)commits.size();
+        int32_t item = 0;
+        for (int ci = 0; ci < nc; ci++) {
+            CommitDev &cm = commits[ci];
+            int64_t p = (int64_t)cm.npos / (4 * sms);
+            p = std::max<int64_t>(256, std::min<int64_t>(2048, p));
+            p = (p + 255) / 256 * 256;
+            cm.p_item = (int32_t)p;
+            cm.pw = (int32_t)(p / kItemWarps);
+            cm.n_items = (int32_t)((cm.npos + p - 1) / p);
+            cm.item_base = item;
+            item += cm.n_items;
+        }
+        n_items = item;
+        // commit DAG
+        std::vector<std::vector<int>> preds(nc);
+        std::vector<int> depth(nc, 0);
+        std::vector<int> prev_sinks;
+        int lv_begin = 0;
+        while (lv_begin < nc) {
+            const int lvl = commits[lv_begin].level;
+            int lv_end = lv_begin;
+            while (lv_end < nc && commits[lv_end].level == lvl) lv_end++;
+            std::vector<bool> has_succ(nc, false);
+            for (int c = lv_begin; c < lv_end; c++) {
+                for (int d : prev_sinks) preds[c].push_back(d);
+                const uint32_t v = c_vmask[c], rd = c_reads[c];
+                int dmax = 0;
+                for (int d = lv_begin; d < c; d++) {
+                    const uint32_t w = c_vmask[d];
+                    bool dep = w == v;  // earlier phase of the same class
+                    for (int a = 0; a < d_rank(); a++)
+                        if ((rd >> a & 1) && (v >> a & 1) && w == (v & ~(1u << a))) dep = true;
+                    if (dep) {
+                        preds[c].push_back(d);
+                        has_succ[d] = true;
+                        dmax = std::max(dmax, depth[d] + 1);
+                    }
+                }
+                depth[c] = dmax;
+            }
+            prev_sinks.clear();
+            for (int c = lv_begin; c < lv_end; c++)
+                if (!has_succ[c]) prev_sinks.push_back(c);
+            lv_begin = lv_end;
+        }
+        // coarse prefix: leading levels whose commits are all tiny
+        c_coarse = 0;
+        {
+            int c = 0;
+            while (c < nc) {
+                int e = c;
+                bool tiny = true;
+                while (e < nc && commits[e].level == commits[c].level) tiny &= commits[e++].npos <= kCoarseMax;
+                if (!tiny) break;
+                c = e;
+            }
+            c_coarse = c;
+        }
+        // coarse schedule: (level, depth) groups of (commit, item) pairs
+        coarse_pairs.clear();
+        coarse_groups.clear();
+        for (int c = 0; c < c_coarse;) {
+            int e = c;
+            while (e < c_coarse && commits[e].level == commits[c].level) e++;
+            int maxd = 0;
+            for (int k = c; k < e; k++) maxd = std::max(maxd, depth[k]);
+            for (int dd = 0; dd <= maxd; dd++) {
+                const int g0 = (int)coarse_pairs.size() / 2;
+                for (int k = c; k < e; k++)
+                    if (depth[k] == dd)
+                        for (int it = 0; it < commits[k].n_items; it++) {
+                            coarse_pairs.push_back(k);
+                            coarse_pairs.push_back(commits[k].item_base + it);
+                        }
+                const int g1 = (int)coarse_pairs.size() / 2;
+                if (g1 > g0) {
+                    coarse_groups.push_back(g0);
+                    coarse_groups.push_back(g1);
+                }
+            }
+            c = e;
+        }
+        // per-item tables and dependency intervals
+        item_commit.assign(n_items, 0);
+        wn.assign((size_t)n_items * kItemWarps, 0);
+        dep_off.assign(n_items + 1, 0);
+        dep_rng.clear();
+        struct Key { int level, depth; int64_t z; int c, it; };
+        std::vector<Key> keys;
+        for (int ci = 0; ci < nc; ci++) {
+            const CommitDev &cm = commits[ci];
+            for (int it = 0; it < cm.n_items; it++) {
+                const int gi = cm.item_base + it;
+                item_commit[gi] = ci;
+                for (int w = 0; w < kItemWarps; w++) {
+                    const int64_t p0 = (int64_t)it * cm.p_item + (int64_t)w * cm.pw;
+                    const int64_t p1 = std::min<int64_t>(p0 + cm.pw, cm.npos);
+                    if (cm.kind == COMMIT_UNIFORM) wn[(size_t)gi * kItemWarps + w] = (int32_t)std::max<int64_t>(0, p1 - p0);
+                }
+                if (cm.kind != COMMIT_UNIFORM) mixed_items.push_back(gi);
+                dep_off[gi] = (int32_t)dep_rng.size();
+                if (ci >= c_coarse) {
+                    for (int d : preds[ci])
+                        if (d >= c_coarse) dep_rng.push_back(dep_interval(cm, it, commits[d]));
+                    const int64_t U = (int64_t)cm.npos / cm.cnt[0];
+                    const int64_t z = cm.start[0] + ((int64_t)it * cm.p_item / U) * (int64_t)cm.step[0];
+                    keys.push_back(Key{cm.level, depth[ci], z, ci, it});
+                }
+            }
+        }
+        dep_off[n_items] = (int32_t)dep_rng.size();
+        std::stable_sort(keys.begin(), keys.end(), [](const Key &a, const Key &b) {
+            if (a.level != b.level) return a.level < b.level;
+            if (a.depth != b.depth) return a.depth < b.depth;
+            if (a.z != b.z) return a.z < b.z;
+            if (a.c != b.c) return a.c < b.c;
+            return a.it < b.it;
+        });
+        flow_order.clear();
+        for (const Key &k : keys) flow_order.push_back(commits[k.c].item_base + k.it);
+        first_flow_item = 0;
+        flow_grid = std::max(1, (int)flow_order.size());  // capped by occupancy at launch
+        coarse_fast = flow_fast = true;
+        for (int ci = 0; ci < nc; ci++) {
+            CommitDev &cm = commits[ci];
+            cm.fast_id = fast_id_of(cm);
+            bool &f = ci < c_coarse ? coarse_fast : flow_fast;
+            f = f && cm.fast_id >= 0;
+        }
+    }
+    int d_rank() const { return d.rank; }
 };
 
 template <typename T>
@@ -890,89 +1503,129 @@ static int cuda_status(cudaError_t e) {
     return HPEZ_CUDA_ERROR;
 }
 
-typedef void (*commit_fn)(const GridDev, const CommitDev, const SweepPtrs);
+typedef void (*sweep_fn)(const SweepArgs);
+
+struct KernelSet {
+    sweep_fn coarse, flow, coarse_fast, flow_fast;  // *_fast null when not instantiated
+};
+
+// Fast rank-3 paths are instantiated for the production element types:
+// f32 grids (ROUND_F32, f32 storage) and f64 grids (ROUND_NONE), u16 codes.
+template <typename T, typename C, int DIR, int ROUND>
+static constexpr bool kFastTypes = (std::is_same<C, uint16_t>::value &&
+                                    ((std::is_same<T, float>::value && ROUND == HPEZ_ROUND_F32) ||
+                                     (std::is_same<T, double>::value && ROUND == HPEZ_ROUND_NONE)));
 
 template <typename T, typename C, int DIR, int ROUND>
-static commit_fn pick3(bool stats, bool mixed) {
-    if (DIR == HPEZ_COMPRESS && stats)
-        return mixed ? commit_kernel<T, C, DIR, ROUND, true, true> : commit_kernel<T, C, DIR, ROUND, true, false>;
-    return mixed ? commit_kernel<T, C, DIR, ROUND, false, true> : commit_kernel<T, C, DIR, ROUND, false, false>;
+static KernelSet pick3(bool stats) {
+    KernelSet k{};
+    if (DIR == HPEZ_COMPRESS && stats) {
+        k.coarse = coarse_kernel<T, C, DIR, ROUND, true, false>;
+        k.flow = flow_kernel<T, C, DIR, ROUND, true, false>;
+        return k;
+    }
+    k.coarse = coarse_kernel<T, C, DIR, ROUND, false, false>;
+    k.flow = flow_kernel<T, C, DIR, ROUND, false, false>;
+    if constexpr (kFastTypes<T, C, DIR, ROUND>) {
+        k.coarse_fast = coarse_kernel<T, C, DIR, ROUND, false, true>;
+        k.flow_fast = flow_kernel<T, C, DIR, ROUND, false, true>;
+    }
+    return k;
 }
 
 template <typename T, typename C>
-static commit_fn pick2(int dir, int round, bool stats, bool mixed) {
+static KernelSet pick2(int dir, int round, bool stats) {
     if (dir == HPEZ_COMPRESS) {
-        if (round == HPEZ_ROUND_F32) return pick3<T, C, HPEZ_COMPRESS, HPEZ_ROUND_F32>(stats, mixed);
-        if (round == HPEZ_ROUND_INT) return pick3<T, C, HPEZ_COMPRESS, HPEZ_ROUND_INT>(stats, mixed);
-        return pick3<T, C, HPEZ_COMPRESS, HPEZ_ROUND_NONE>(stats, mixed);
+        if (round == HPEZ_ROUND_F32) return pick3<T, C, HPEZ_COMPRESS, HPEZ_ROUND_F32>(stats);
+        if (round == HPEZ_ROUND_INT) return pick3<T, C, HPEZ_COMPRESS, HPEZ_ROUND_INT>(stats);
+        return pick3<T, C, HPEZ_COMPRESS, HPEZ_ROUND_NONE>(stats);
     }
-    if (round == HPEZ_ROUND_F32) return pick3<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_F32>(false, mixed);
-    if (round == HPEZ_ROUND_INT) return pick3<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_INT>(false, mixed);
-    return pick3<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_NONE>(false, mixed);
+    if (round == HPEZ_ROUND_F32) return pick3<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_F32>(false);
+    if (round == HPEZ_ROUND_INT) return pick3<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_INT>(false);
+    return pick3<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_NONE>(false);
 }
 
-static commit_fn pick(const hpez_sweep_desc &d, bool mixed) {
+static KernelSet pick(const hpez_sweep_desc &d) {
     const bool stats = d.with_stats != 0;
     if (d.work_dtype == HPEZ_WORK_F32) {
-        if (d.code_dtype == HPEZ_CODES_U16) return pick2<float, uint16_t>(d.direction, d.rounding, stats, mixed);
-        return pick2<float, int32_t>(d.direction, d.rounding, stats, mixed);
+        if (d.code_dtype == HPEZ_CODES_U16) return pick2<float, uint16_t>(d.direction, d.rounding, stats);
+        return pick2<float, int32_t>(d.direction, d.rounding, stats);
     }
-    if (d.code_dtype == HPEZ_CODES_U16) return pick2<double, uint16_t>(d.direction, d.rounding, stats, mixed);
-    return pick2<double, int32_t>(d.direction, d.rounding, stats, mixed);
+    if (d.code_dtype == HPEZ_CODES_U16) return pick2<double, uint16_t>(d.direction, d.rounding, stats);
+    return pick2<double, int32_t>(d.direction, d.rounding, stats);
+}
+
+static SweepArgs base_args(Plan &p) {
+    SweepArgs A{};
+    A.g = p.g;
+    A.commits = p.d_commits;
+    A.item_commit = p.d_item_commit;
+    A.flow_order = p.d_flow_order;
+    A.dep_off = p.d_dep_off;
+    A.dep_rng = p.d_dep_rng;
+    A.coarse_pairs = p.d_coarse_pairs;
+    A.coarse_groups = p.d_coarse_groups;
+    A.n_groups = (int32_t)(p.coarse_groups.size() / 2);
+    A.wbase = p.d_wbase;
+    A.wn = p.d_wn;
+    A.esc_cnt = p.d_esc_cnt;
+    A.esc_off = p.d_esc_off;
+    A.done = p.d_done;
+    A.next = p.d_counters;
+    A.flags = p.d_counters + 1;
+    A.tags = p.d_tags;
+    A.slots = p.d_slots;
+    A.table = p.d_table;
+    return A;
 }
 
 static int plan_setup(Plan *p, cudaStream_t st) {
-    // device metadata, once per plan
     cudaError_t e = cudaSuccess;
-    const size_t nb = (size_t)std::max<int64_t>(p->total_blocks, 1);
-    e = dalloc(&p->d_status, nb);
+    const size_t ni = (size_t)std::max(p->n_items, 1);
+    const size_t ne = ni * kItemWarps;
+    const size_t ntiles = (ne + kScanTile - 1) / kScanTile + 1;
+    e = dupload(&p->d_commits, p->commits);
+    if (!e) e = dupload(&p->d_item_commit, p->item_commit);
+    if (!e) e = dupload(&p->d_flow_order, p->flow_order);
+    if (!e) e = dupload(&p->d_dep_off, p->dep_off);
+    if (!e) e = dupload(&p->d_dep_rng, p->dep_rng);
+    if (!e) e = dupload(&p->d_coarse_pairs, p->coarse_pairs);
+    if (!e) e = dupload(&p->d_coarse_groups, p->coarse_groups);
+    if (!e) e = dupload(&p->d_wn, p->wn);
+    if (!e) e = dalloc(&p->d_wbase, ne);
+    if (!e) e = dalloc(&p->d_esc_cnt, ne);
+    if (!e) e = dalloc(&p->d_esc_off, ne);
+    if (!e) e = dalloc(&p->d_scan_tmp, ntiles);
+    if (!e) e = dalloc(&p->d_total, 4);
+    if (!e) e = dalloc(&p->d_done, ni);
     if (!e) e = dalloc(&p->d_counters, 4);
-    if (!e) e = dalloc(&p->d_blkoff, nb);
-    if (!e && p->has_mixed) e = dalloc(&p->d_blkcnt, nb);
     if (!e) e = dupload(&p->d_tags, p->tags);
     if (!e) e = dupload(&p->d_slots, p->slots);
     if (!e) e = dupload(&p->d_table, p->table);
-    if (!e) e = dupload(&p->d_classes, p->classes);
-    const size_t nc = p->commits.size();
-    std::vector<int64_t> cblk(nc), cnblk(nc), cbase(nc), cn(nc);
-    std::vector<int32_t> clevel(nc);
-    for (size_t i = 0; i < nc; i++) {
-        cblk[i] = p->commits[i].blk_base;
-        cnblk[i] = p->commits[i].nblocks;
-        cbase[i] = p->commits[i].code_base;
-        cn[i] = p->commits[i].kind == COMMIT_UNIFORM ? (int64_t)p->commits[i].npos : 0;
-        clevel[i] = p->commits[i].level;
-    }
-    if (!e) e = dupload(&p->d_cblk, cblk);
-    if (!e) e = dupload(&p->d_cnblk, cnblk);
-    if (!e) e = dupload(&p->d_cbase, cbase);
-    if (!e) e = dupload(&p->d_cn, cn);
+    if (!e) e = dupload(&p->d_mixed_items, p->mixed_items);
+    const size_t nc = std::max<size_t>(p->commits.size(), 1);
+    std::vector<int32_t> clevel(nc, 0);
+    for (size_t i = 0; i < p->commits.size(); i++) clevel[i] = p->commits[i].level;
     if (!e) e = dupload(&p->d_clevel, clevel);
+    if (!e) e = dalloc(&p->d_cbase, nc);
+    if (!e) e = dalloc(&p->d_cn, nc);
     if (e) return cuda_status(e);
-    if (p->has_mixed) {
-        for (const CommitDev &cm : p->commits) {
-            if (cm.kind == COMMIT_UNIFORM) continue;
-            mixed_count_kernel<<<cm.nblocks, kThreads, 0, st>>>(p->g, cm, p->d_table, p->d_tags,
-                                                                p->d_slots, p->d_blkcnt);
-        }
-        mixed_scan_kernel<<<(unsigned)p->classes.size(), 1024, 0, st>>>(
-            p->d_classes, p->d_cblk, p->d_cnblk, p->d_blkcnt, p->d_blkoff, p->d_cbase, p->d_cn);
-        e = cudaGetLastError();
-        if (e) return cuda_status(e);
+    SweepArgs A = base_args(*p);
+    if (!p->mixed_items.empty()) {
+        const int64_t thr = (int64_t)p->mixed_items.size() * kItemWarps * 32;
+        mixed_count_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(A, p->d_wn, (int32_t)p->mixed_items.size(),
+                                                                         p->d_mixed_items);
     }
+    // code index of every (item, warp)'s first member = exclusive scan of member counts
+    if (p->n_items > 0)
+        exclusive_scan(p->d_wn, (int64_t)p->n_items * kItemWarps, p->d_wbase, p->d_scan_tmp, p->d_total, st);
+    if (!p->commits.empty())
+        commit_ranges_kernel<<<(unsigned)((p->commits.size() + 127) / 128), 128, 0, st>>>(
+            p->d_commits, (int)p->commits.size(), p->d_wbase, p->d_wn, p->d_cbase, p->d_cn);
+    e = cudaGetLastError();
+    if (e) return cuda_status(e);
     if (p->d.with_stats && p->d.direction == HPEZ_COMPRESS) {
-        // leaf offsets per commit (upper bound n/64 + 1 leaves each)
-        std::vector<int64_t> loff(nc + 1, 0);
-        int64_t tot = 0;
-        for (size_t i = 0; i < nc; i++) {
-            loff[i] = tot;
-            tot += (int64_t)p->commits[i].npos / 64 + 2;
-        }
-        loff[nc] = tot;
-        p->leaf_total = tot;
-        e = dupload(&p->d_leafoff, loff);
-        if (!e) e = dalloc(&p->d_leaves, (size_t)tot);
-        if (!e) e = dalloc(&p->d_csum, nc);
+        e = dalloc(&p->d_csum, nc);
         if (!e) e = dalloc(&p->d_errbuf, (size_t)std::max<int64_t>(p->num_codes, 1));
         if (e) return cuda_status(e);
     }
@@ -992,8 +1645,7 @@ extern "C" {
 
 int hpez_plan_create(const hpez_sweep_desc *desc, hpez_plan *out) {
     if (!desc || !out) return HPEZ_BAD_ARGUMENT;
-    if (desc->rank < 1 || desc->rank > kMaxRank || desc->n_levels < 0 ||
-        (desc->n_levels > 0 && !desc->levels))
+    if (desc->rank < 1 || desc->rank > kMaxRank || desc->n_levels < 0 || (desc->n_levels > 0 && !desc->levels))
         return HPEZ_BAD_ARGUMENT;
     std::unique_ptr<hpez_plan_s> h(new hpez_plan_s());
     Plan &p = h->p;
@@ -1017,7 +1669,18 @@ int hpez_plan_destroy(hpez_plan plan) {
 
 int64_t hpez_plan_num_codes(hpez_plan plan) { return plan ? plan->p.num_codes : -1; }
 int32_t hpez_plan_num_commits(hpez_plan plan) { return plan ? (int32_t)plan->p.commits.size() : -1; }
-int32_t hpez_plan_num_launches(hpez_plan plan) { return plan ? (int32_t)plan->p.commits.size() : -1; }
+
+int32_t hpez_plan_num_launches(hpez_plan plan) {
+    if (!plan) return -1;
+    const Plan &p = plan->p;
+    int n = 0;
+    if (!p.coarse_groups.empty()) n++;
+    if (!p.flow_order.empty()) n++;
+    n += 3;  // escape scan (3 kernels)
+    n += 1;  // escape count pre-pass (decompress) or outlier gather (compress)
+    if (p.d.with_stats && p.d.direction == HPEZ_COMPRESS) n += 2;
+    return n;
+}
 
 int hpez_plan_level_codes(hpez_plan plan, int64_t *out) {
     if (!plan || !out) return HPEZ_BAD_ARGUMENT;
@@ -1029,53 +1692,80 @@ int hpez_set_device(int32_t device) { return cuda_status(cudaSetDevice(device));
 
 const char *hpez_build_info(void) { return "libhpez_b200 sm_100a f64 -fmad=false"; }
 
-int hpez_sweep_run(hpez_plan plan, void *work, void *codes, int64_t codes_avail, double *outliers,
-                   int64_t outl_cap, double *stat_err_sum, int64_t *stat_count, double *stat_dense,
-                   void *stream) {
+int hpez_sweep_run(hpez_plan plan, void *work, void *codes, int64_t codes_avail, double *outliers, int64_t outl_cap,
+                   double *stat_err_sum, int64_t *stat_count, double *stat_dense, void *stream) {
     if (!plan || !work) return HPEZ_BAD_ARGUMENT;
     Plan &p = plan->p;
     cudaStream_t st = (cudaStream_t)stream;
     if (p.d.direction == HPEZ_DECOMPRESS && codes_avail < p.num_codes) return HPEZ_CORRUPT_STREAM;
     if (p.num_codes > 0 && !codes) return HPEZ_BAD_ARGUMENT;
-    if (p.d.with_stats && p.d.direction == HPEZ_COMPRESS && (!stat_err_sum || !stat_count))
-        return HPEZ_BAD_ARGUMENT;
+    const bool stats = p.d.with_stats && p.d.direction == HPEZ_COMPRESS;
+    if (stats && (!stat_err_sum || !stat_count)) return HPEZ_BAD_ARGUMENT;
     if (!p.setup_done) {
         int s = plan_setup(&p, st);
         if (s) return s;
     }
-    cudaError_t e = cudaMemsetAsync(p.d_status, 0, sizeof(uint64_t) * std::max<int64_t>(p.total_blocks, 1), st);
-    if (!e) e = cudaMemsetAsync(p.d_counters, 0, 4 * sizeof(unsigned long long), st);
+    const int64_t ne = (int64_t)p.n_items * kItemWarps;
+    cudaError_t e = cudaMemsetAsync(p.d_counters, 0, 4 * sizeof(int32_t), st);
+    if (!e) e = cudaMemsetAsync(p.d_total, 0, sizeof(int64_t), st);
     if (e) return cuda_status(e);
-    SweepPtrs P{};
-    P.work = work;
-    P.codes = codes;
-    P.outl = outliers;
-    P.outl_cap = outliers ? outl_cap : 0;
-    P.status = p.d_status;
-    P.ticket = p.d_counters;
-    P.flags = (int32_t *)(p.d_counters + 1);
-    P.blkoff = p.d_blkoff;
-    P.tags = p.d_tags;
-    P.slots = p.d_slots;
-    P.table = p.d_table;
-    P.errbuf = p.d_errbuf;
-    P.dense = stat_dense;
-    const commit_fn fu = pick(p.d, false), fm = pick(p.d, true);
-    for (const CommitDev &cm : p.commits) {
-        commit_fn f = cm.kind == COMMIT_UNIFORM ? fu : fm;
-        f<<<cm.nblocks, kThreads, 0, st>>>(p.g, cm, P);
+    if (p.n_items == 0) {  // no commits (e.g. a grid made of anchors only)
+        p.outl_cap_last = outliers ? outl_cap : 0;
+        return HPEZ_OK;
+    }
+    e = cudaMemsetAsync(p.d_done, 0, sizeof(uint32_t) * (size_t)p.n_items, st);
+    if (e) return cuda_status(e);
+    SweepArgs A = base_args(p);
+    A.work = work;
+    A.codes = codes;
+    A.outl = outliers;
+    A.outl_cap = outliers ? outl_cap : 0;
+    A.errbuf = p.d_errbuf;
+    A.dense = stat_dense;
+    const KernelSet ks = pick(p.d);
+    if (p.d.direction == HPEZ_DECOMPRESS) {
+        // outlier ranks: zero codes per (item, warp), then an exclusive scan
+        const int64_t thr = ne * 32;
+        if (p.d.code_dtype == HPEZ_CODES_U16)
+            count_zero_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>((const uint16_t *)codes, p.d_wbase, p.d_wn,
+                                                                             ne, p.d_esc_cnt);
+        else
+            count_zero_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>((const int32_t *)codes, p.d_wbase, p.d_wn,
+                                                                             ne, p.d_esc_cnt);
+        exclusive_scan(p.d_esc_cnt, ne, p.d_esc_off, p.d_scan_tmp, p.d_total, st);
+    }
+    if (!p.coarse_groups.empty()) {
+        sweep_fn f = (p.coarse_fast && ks.coarse_fast) ? ks.coarse_fast : ks.coarse;
+        f<<<1, 1024, 0, st>>>(A);
+    }
+    if (!p.flow_order.empty()) {
+        A.n_items = (int32_t)p.flow_order.size();
+        sweep_fn f = (p.flow_fast && ks.flow_fast) ? ks.flow_fast : ks.flow;
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kItemThreads, 0) != cudaSuccess || occ < 1) occ = 1;
+        const int grid = std::min(p.flow_grid, occ * num_sms());
+        f<<<grid, kItemThreads, 0, st>>>(A);
     }
     e = cudaGetLastError();
     if (e) return cuda_status(e);
-    if (p.d.with_stats && p.d.direction == HPEZ_COMPRESS && !p.commits.empty()) {
-        commit_pairwise_kernel<<<(unsigned)p.commits.size(), 32, 0, st>>>(
-            p.d_errbuf, p.d_cbase, p.d_cn, p.d_csum, p.d_leaves, p.d_leafoff);
-        stats_accumulate_kernel<<<1, 32, 0, st>>>((int)p.commits.size(), p.d_clevel, p.d_csum,
-                                                  p.d_cn, stat_err_sum, stat_count);
-        e = cudaGetLastError();
-        if (e) return cuda_status(e);
+    if (p.d.direction == HPEZ_COMPRESS) {
+        exclusive_scan(p.d_esc_cnt, ne, p.d_esc_off, p.d_scan_tmp, p.d_total, st);
+        const int64_t thr = ne * 32;
+        auto *gk = p.d.work_dtype == HPEZ_WORK_F32
+                       ? (p.d.code_dtype == HPEZ_CODES_U16 ? gather_outliers_kernel<float, uint16_t>
+                                                           : gather_outliers_kernel<float, int32_t>)
+                       : (p.d.code_dtype == HPEZ_CODES_U16 ? gather_outliers_kernel<double, uint16_t>
+                                                           : gather_outliers_kernel<double, int32_t>);
+        gk<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(A, ne, outliers, A.outl_cap);
     }
-    p.outl_cap_last = P.outl_cap;
+    if (stats && !p.commits.empty()) {
+        commit_pairwise_kernel<<<(unsigned)p.commits.size(), 32, 0, st>>>(p.d_errbuf, p.d_cbase, p.d_cn, p.d_csum);
+        stats_accumulate_kernel<<<1, 32, 0, st>>>((int)p.commits.size(), p.d_clevel, p.d_csum, p.d_cn, stat_err_sum,
+                                                  stat_count);
+    }
+    e = cudaGetLastError();
+    if (e) return cuda_status(e);
+    p.outl_cap_last = A.outl_cap;
     return HPEZ_OK;
 }
 
@@ -1086,12 +1776,10 @@ int hpez_sweep_finish(hpez_plan plan, void *stream, int64_t *n_outliers) {
     if (e) return cuda_status(e);
     int64_t n_out = 0;
     int32_t flags = 0;
-    if (p.total_blocks > 0 && p.setup_done) {
-        uint64_t last = 0;
-        e = cudaMemcpy(&last, p.d_status + p.total_blocks - 1, sizeof last, cudaMemcpyDeviceToHost);
+    if (p.setup_done) {
+        e = cudaMemcpy(&n_out, p.d_total, sizeof n_out, cudaMemcpyDeviceToHost);
         if (!e) e = cudaMemcpy(&flags, p.d_counters + 1, sizeof flags, cudaMemcpyDeviceToHost);
         if (e) return cuda_status(e);
-        n_out = (int64_t)(last & kValMask);
     }
     if (n_outliers) *n_outliers = n_out;
     if (flags) return flags;
