@@ -140,6 +140,11 @@ int hpez_rows_pairwise_sum(const double *rows, int64_t nrows, int64_t rowlen, do
  * level li owns codes [out[li], out[li+1]) -- PassStats.code_chunks. */
 int hpez_plan_level_codes(hpez_plan plan, int64_t *out);
 
+/* Plan diagnostics (12 int64): item counts, schedule flags and, when the
+ * environment variable HPEZ_PROFILE is set at plan creation, the flow
+ * kernel's clock64 phase counters (grab, wait, work, units). */
+int hpez_plan_info(hpez_plan plan, int64_t *out);
+
 /* Select the CUDA device for subsequent calls from this host thread. */
 int hpez_set_device(int32_t device);
 

@@ -21,6 +21,7 @@
 //     decompress ranks them with a counting pre-pass over the code stream.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -127,9 +128,12 @@ static cudaError_t upload_rows() {
 }
 
 // ---------------------------------------------------------- predictions --
+// Grid reads go through L1: a unit starts only after a gpu-scope fence that
+// invalidates this SM's L1 (MEMBAR.SC.GPU + CCTL.IVALL) and reads only points
+// finalised by the commits it waited on.
 template <typename T>
 __device__ __forceinline__ double ldv(const T *__restrict__ w, int64_t i) {
-    return (double)__ldcg(w + i);
+    return (double)w[i];
 }
 
 #define DM(a, b) __dmul_rn((a), (b))
@@ -255,6 +259,7 @@ struct SweepArgs {
     const int32_t *coarse_pairs;  // (commit, item) pairs of the coarse prefix
     const int32_t *coarse_groups; // [g0, g1) pair ranges, one per (level, depth)
     int32_t n_groups;
+    unsigned long long *prof;   // optional phase counters (HPEZ_PROFILE)
     const int64_t *wbase;       // per (item, warp): code index of the first member
     const int32_t *wn;          // per (item, warp): member count
     uint32_t *esc_cnt;          // per (item, warp): escapes (compress, written)
@@ -423,33 +428,46 @@ __device__ __forceinline__ void process_warp(const SweepArgs &A, const CommitDev
 // (0,1,2).  Geometry is held in registers and lattice indices advance
 // incrementally, so the per-point cost is the stencil, the quantizer and a
 // few integer operations.
+// 1-D row of family FAM at coordinate c (extent E, stride s, element step sE)
+// with every edge truncation of kernels.resolve_row (kernels.py:106-150)
+// written out: inter-level cubic rows try (-1,1,3), (-3,-1,1), (-1,1),
+// (-3,-1), (-1,); same-level rows (-2,-1,1,2), (-2,-1,1), (-2,-1); a
+// truncated 6-point natural row falls back to the 4-point not-a-knot row.
 template <int FAM, typename T>
 __device__ __forceinline__ double p1d(const T *__restrict__ w, int idx, int c, int E, int s, int sE) {
+    auto v = [&](int u) { return (double)w[idx + u * sE]; };
+    const bool r1 = c + s <= E - 1;
     if (FAM == FAM_LIN_I) {
-        if (c + s <= E - 1) return DA(DM(0.5, ldv(w, idx - sE)), DM(0.5, ldv(w, idx + sE)));
-        return DM(1.0, ldv(w, idx - sE));
+        if (r1) return DA(DM(0.5, v(-1)), DM(0.5, v(1)));
+        return DM(1.0, v(-1));
     }
     if (FAM == FAM_NAK_I || FAM == FAM_NAT_I) {
-        if (c >= 3 * s && c + 3 * s <= E - 1) {
-            const double a = ldv(w, idx - 3 * sE), b = ldv(w, idx - sE), d = ldv(w, idx + sE), e = ldv(w, idx + 3 * sE);
+        const bool l3 = c >= 3 * s, r3 = c + 3 * s <= E - 1;
+        if (l3 && r3) {
+            const double a = v(-3), b = v(-1), d = v(1), e = v(3);
             if (FAM == FAM_NAK_I)
                 return DA(DA(DA(DM(-1.0 / 16, a), DM(9.0 / 16, b)), DM(9.0 / 16, d)), DM(-1.0 / 16, e));
             return DA(DA(DA(DM(-3.0 / 40, a), DM(23.0 / 40, b)), DM(23.0 / 40, d)), DM(-3.0 / 40, e));
         }
-    } else if (FAM == FAM_NAK_S) {
-        if (c + 2 * s <= E - 1) {
-            const double a = ldv(w, idx - 2 * sE), b = ldv(w, idx - sE), d = ldv(w, idx + sE), e = ldv(w, idx + 2 * sE);
-            return DA(DA(DA(DM(-1.0 / 6, a), DM(4.0 / 6, b)), DM(4.0 / 6, d)), DM(-1.0 / 6, e));
-        }
-    } else {
-        if (c + 3 * s <= E - 1) {
-            const double a = ldv(w, idx - 3 * sE), b = ldv(w, idx - 2 * sE), d = ldv(w, idx - sE),
-                         e = ldv(w, idx + sE), f = ldv(w, idx + 2 * sE), h = ldv(w, idx + 3 * sE);
-            return DA(DA(DA(DA(DA(DM(3.0 / 62, a), DM(-18.0 / 62, b)), DM(46.0 / 62, d)), DM(46.0 / 62, e)),
-                         DM(-18.0 / 62, f)), DM(3.0 / 62, h));
-        }
+        if (r3) return DA(DA(DM(3.0 / 8, v(-1)), DM(3.0 / 4, v(1))), DM(-1.0 / 8, v(3)));
+        if (l3 && r1) return DA(DA(DM(-1.0 / 8, v(-3)), DM(3.0 / 4, v(-1))), DM(3.0 / 8, v(1)));
+        if (r1) return DA(DM(0.5, v(-1)), DM(0.5, v(1)));
+        if (l3) return DA(DM(-0.5, v(-3)), DM(1.5, v(-1)));
+        return DM(1.0, v(-1));
     }
-    return pred_table(w, (int64_t)idx, c, E, s, (int64_t)sE, FAM);
+    // same-level families: targets sit at >= 3s, so only the right side truncates
+    const bool r2 = c + 2 * s <= E - 1;
+    if (FAM == FAM_NAT_S && c + 3 * s <= E - 1) {
+        const double a = v(-3), b = v(-2), d = v(-1), e = v(1), f = v(2), h = v(3);
+        return DA(DA(DA(DA(DA(DM(3.0 / 62, a), DM(-18.0 / 62, b)), DM(46.0 / 62, d)), DM(46.0 / 62, e)),
+                     DM(-18.0 / 62, f)), DM(3.0 / 62, h));
+    }
+    if (r2) {
+        const double a = v(-2), b = v(-1), d = v(1), e = v(2);
+        return DA(DA(DA(DM(-1.0 / 6, a), DM(4.0 / 6, b)), DM(4.0 / 6, d)), DM(-1.0 / 6, e));
+    }
+    if (r1) return DA(DA(DM(-1.0 / 3, v(-2)), DM(1.0, v(-1))), DM(1.0 / 3, v(1)));
+    return DA(DM(-1.0, v(-2)), DM(2.0, v(-1)));
 }
 
 template <typename T, typename C, int DIR, int ROUND, int KIND, int FAM>
@@ -593,7 +611,9 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? 4 : 3) flow_kernel(const 
     __shared__ int s_item;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int cur = -1;
+    unsigned long long t_grab = 0, t_wait = 0, t_work = 0, n_done = 0;
     while (true) {
+        const long long c0 = A.prof ? clock64() : 0;
         if (threadIdx.x == 0) s_item = atomicAdd(A.next, 1);
         __syncthreads();
         const int rel = s_item;
@@ -605,6 +625,7 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? 4 : 3) flow_kernel(const 
                 ((uint32_t *)&s_cm)[threadIdx.x] = ((const uint32_t *)&A.commits[c])[threadIdx.x];
             cur = c;
         }
+        const long long c1 = A.prof ? clock64() : 0;
         if (warp == 0) {
             const int k0 = A.dep_off[item], k1 = A.dep_off[item + 1];
             for (int k = k0; k < k1; k++) {
@@ -612,14 +633,28 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? 4 : 3) flow_kernel(const 
                 for (int q = d.x + lane; q <= d.y; q += 32)
                     while (ld_relaxed(&A.done[q]) == 0) __nanosleep(32);
             }
-            __threadfence();
+            __threadfence();  // also invalidates this SM's L1 (CCTL.IVALL)
         }
         __syncthreads();
+        const long long c2 = A.prof ? clock64() : 0;
         if (FAST) process_dispatch<T, C, DIR, ROUND>(A, s_cm, item, warp);
         else process_warp<T, C, DIR, ROUND, STATS>(A, s_cm, item, warp);
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) st_release(&A.done[item], 1u);
+        if (A.prof) {
+            const long long c3 = clock64();
+            t_grab += c1 - c0;
+            t_wait += c2 - c1;
+            t_work += c3 - c2;
+            n_done++;
+        }
+    }
+    if (A.prof && threadIdx.x == 0) {
+        atomicAdd(A.prof + 0, t_grab);
+        atomicAdd(A.prof + 1, t_wait);
+        atomicAdd(A.prof + 2, t_work);
+        atomicAdd(A.prof + 3, n_done);
     }
 }
 
@@ -971,7 +1006,7 @@ struct Plan {
     std::vector<int64_t> level_codes;
     int32_t n_items = 0;
     int32_t c_coarse = 0;      // commits [0, c_coarse) run in the coarse kernel
-    bool coarse_fast = false, flow_fast = false;
+    bool coarse_fast = false, flow_fast = false, diag_order = false;
     int32_t first_flow_item = 0;
     std::vector<int32_t> item_commit;
     std::vector<int32_t> dep_off;     // per item: first entry in dep_rng
@@ -1003,12 +1038,13 @@ struct Plan {
     int64_t *d_cbase = nullptr, *d_cn = nullptr;
     int32_t *d_clevel = nullptr;
     double *d_errbuf = nullptr, *d_csum = nullptr;
+    unsigned long long *d_prof = nullptr;
     bool setup_done = false;
     int64_t outl_cap_last = 0;
     int flow_grid = 0;
 
     ~Plan() {
-        void *ptrs[] = {d_commits, d_item_commit, d_flow_order, d_dep_off, d_coarse_pairs, d_coarse_groups,
+        void *ptrs[] = {d_prof, d_commits, d_item_commit, d_flow_order, d_dep_off, d_coarse_pairs, d_coarse_groups,
                         d_dep_rng, d_wbase, d_wn, d_esc_cnt, d_esc_off,
                         d_scan_tmp, d_total, d_done, d_counters, d_tags, d_slots, d_table,
                         d_mixed_items, d_cbase, d_cn, d_clevel, d_errbuf, d_csum};
@@ -1462,15 +1498,50 @@ struct Plan {
             }
         }
         dep_off[n_items] = (int32_t)dep_rng.size();
-        std::stable_sort(keys.begin(), keys.end(), [](const Key &a, const Key &b) {
-            if (a.level != b.level) return a.level < b.level;
-            if (a.depth != b.depth) return a.depth < b.depth;
-            if (a.z != b.z) return a.z < b.z;
-            if (a.c != b.c) return a.c < b.c;
-            return a.it < b.it;
-        });
-        flow_order.clear();
-        for (const Key &k : keys) flow_order.push_back(commits[k.c].item_base + k.it);
+        // Diagonal (wavefront) order within a level: key z + depth * W with W
+        // wider than any dependency reach, so an item's dependencies are
+        // always grabbed before it while the in-flight band of planes stays
+        // small enough to live in L2.  Verified below; depth-major fallback.
+        std::vector<int64_t> wlev(64, 0);
+        for (const Key &k : keys) {
+            const CommitDev &cm = commits[k.c];
+            const int64_t U = (int64_t)cm.npos / cm.cnt[0];
+            const int64_t pa = (int64_t)k.it * cm.p_item;
+            const int64_t pb = std::min<int64_t>(pa + cm.p_item, cm.npos) - 1;
+            const int64_t span = ((pb / U) - (pa / U)) * (int64_t)cm.step[0];
+            wlev[k.level & 63] = std::max<int64_t>(wlev[k.level & 63], span + 7 * (int64_t)cm.s + 2 * cm.step[0] + 1);
+        }
+        auto order_by = [&](bool diag) {
+            std::vector<Key> ks = keys;
+            std::stable_sort(ks.begin(), ks.end(), [&](const Key &a, const Key &b) {
+                if (a.level != b.level) return a.level < b.level;
+                if (diag) {
+                    const int64_t ka = a.z + a.depth * wlev[a.level & 63], kb = b.z + b.depth * wlev[b.level & 63];
+                    if (ka != kb) return ka < kb;
+                }
+                if (a.depth != b.depth) return a.depth < b.depth;
+                if (a.z != b.z) return a.z < b.z;
+                if (a.c != b.c) return a.c < b.c;
+                return a.it < b.it;
+            });
+            std::vector<int32_t> ord;
+            for (const Key &k : ks) ord.push_back(commits[k.c].item_base + k.it);
+            return ord;
+        };
+        auto valid = [&](const std::vector<int32_t> &ord) {
+            std::vector<int32_t> pos(n_items, -1);
+            for (size_t i = 0; i < ord.size(); i++) pos[ord[i]] = (int32_t)i;
+            for (size_t i = 0; i < ord.size(); i++) {
+                const int it = ord[i];
+                for (int k = dep_off[it]; k < dep_off[it + 1]; k++)
+                    for (int q = dep_rng[k].x; q <= dep_rng[k].y; q++)
+                        if (pos[q] < 0 || pos[q] >= (int32_t)i) return false;
+            }
+            return true;
+        };
+        flow_order = order_by(true);
+        diag_order = valid(flow_order);
+        if (!diag_order) flow_order = order_by(false);
         first_flow_item = 0;
         flow_grid = std::max(1, (int)flow_order.size());  // capped by occupancy at launch
         coarse_fast = flow_fast = true;
@@ -1566,6 +1637,7 @@ static SweepArgs base_args(Plan &p) {
     A.coarse_pairs = p.d_coarse_pairs;
     A.coarse_groups = p.d_coarse_groups;
     A.n_groups = (int32_t)(p.coarse_groups.size() / 2);
+    A.prof = p.d_prof;
     A.wbase = p.d_wbase;
     A.wn = p.d_wn;
     A.esc_cnt = p.d_esc_cnt;
@@ -1603,6 +1675,10 @@ static int plan_setup(Plan *p, cudaStream_t st) {
     if (!e) e = dupload(&p->d_slots, p->slots);
     if (!e) e = dupload(&p->d_table, p->table);
     if (!e) e = dupload(&p->d_mixed_items, p->mixed_items);
+    if (!e && getenv("HPEZ_PROFILE")) {
+        e = dalloc(&p->d_prof, 8);
+        if (!e) e = cudaMemset(p->d_prof, 0, 8 * sizeof(unsigned long long));
+    }
     const size_t nc = std::max<size_t>(p->commits.size(), 1);
     std::vector<int32_t> clevel(nc, 0);
     for (size_t i = 0; i < p->commits.size(); i++) clevel[i] = p->commits[i].level;
@@ -1680,6 +1756,30 @@ int32_t hpez_plan_num_launches(hpez_plan plan) {
     n += 1;  // escape count pre-pass (decompress) or outlier gather (compress)
     if (p.d.with_stats && p.d.direction == HPEZ_COMPRESS) n += 2;
     return n;
+}
+
+// Diagnostics: [n_items, n_flow_items, coarse_commits, coarse_groups,
+// diag_order, flow_fast, coarse_fast, dep_intervals] and, when the plan was
+// built with HPEZ_PROFILE set, the flow kernel's accumulated clock64 phase
+// counters [grab, wait, work, items] (out[8..11]).
+int hpez_plan_info(hpez_plan plan, int64_t *out) {
+    if (!plan || !out) return HPEZ_BAD_ARGUMENT;
+    const Plan &p = plan->p;
+    out[0] = p.n_items;
+    out[1] = (int64_t)p.flow_order.size();
+    out[2] = p.c_coarse;
+    out[3] = (int64_t)p.coarse_groups.size() / 2;
+    out[4] = p.diag_order;
+    out[5] = p.flow_fast;
+    out[6] = p.coarse_fast;
+    out[7] = (int64_t)p.dep_rng.size();
+    for (int i = 8; i < 12; i++) out[i] = -1;
+    if (p.d_prof) {
+        unsigned long long h[4];
+        if (cudaMemcpy(h, p.d_prof, sizeof h, cudaMemcpyDeviceToHost) == cudaSuccess)
+            for (int i = 0; i < 4; i++) out[8 + i] = (int64_t)h[i];
+    }
+    return HPEZ_OK;
 }
 
 int hpez_plan_level_codes(hpez_plan plan, int64_t *out) {
