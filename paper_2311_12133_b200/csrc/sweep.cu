@@ -639,9 +639,11 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? 4 : 3) flow_kernel(const 
         const long long c2 = A.prof ? clock64() : 0;
         if (FAST) process_dispatch<T, C, DIR, ROUND>(A, s_cm, item, warp);
         else process_warp<T, C, DIR, ROUND, STATS>(A, s_cm, item, warp);
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) st_release(&A.done[item], 1u);
+        __syncthreads();  // CTA writes happen-before thread 0's gpu-scope release
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release(&A.done[item], 1u);
+        }
         if (A.prof) {
             const long long c3 = clock64();
             t_grab += c1 - c0;
@@ -987,7 +989,8 @@ static int num_sms() {
     return sms;
 }
 
-constexpr uint32_t kCoarseMax = 4096;  // commits at most this large run in the coarse CTA
+constexpr uint32_t kCoarseMax = 512;  // leading levels whose commits are all this small run in the coarse CTA
+static int kDiagScale = 2;  // commits at most this large run in the coarse CTA
 
 struct Plan {
     hpez_sweep_desc d{};
@@ -1386,12 +1389,17 @@ struct Plan {
     // coordinate) order, so independent commits run concurrently.
     void build_items() {
         const int sms = num_sms();
+        if (const char *ev = getenv("HPEZ_DIAG_SCALE")) kDiagScale = std::max(1, atoi(ev));
+        int pmax = 4096;
+        if (const char *ev = getenv("HPEZ_ITEM_MAX")) pmax = std::max(256, atoi(ev));
+        uint32_t coarse_max = kCoarseMax;
+        if (const char *ev = getenv("HPEZ_COARSE_MAX")) coarse_max = (uint32_t)atoi(ev);
         const int nc = (int)commits.size();
         int32_t item = 0;
         for (int ci = 0; ci < nc; ci++) {
             CommitDev &cm = commits[ci];
             int64_t p = (int64_t)cm.npos / (4 * sms);
-            p = std::max<int64_t>(256, std::min<int64_t>(2048, p));
+            p = std::max<int64_t>(256, std::min<int64_t>(pmax, p));
             p = (p + 255) / 256 * 256;
             cm.p_item = (int32_t)p;
             cm.pw = (int32_t)(p / kItemWarps);
@@ -1439,7 +1447,7 @@ struct Plan {
             while (c < nc) {
                 int e = c;
                 bool tiny = true;
-                while (e < nc && commits[e].level == commits[c].level) tiny &= commits[e++].npos <= kCoarseMax;
+                while (e < nc && commits[e].level == commits[c].level) tiny &= commits[e++].npos <= coarse_max;
                 if (!tiny) break;
                 c = e;
             }
@@ -1509,7 +1517,7 @@ struct Plan {
             const int64_t pa = (int64_t)k.it * cm.p_item;
             const int64_t pb = std::min<int64_t>(pa + cm.p_item, cm.npos) - 1;
             const int64_t span = ((pb / U) - (pa / U)) * (int64_t)cm.step[0];
-            wlev[k.level & 63] = std::max<int64_t>(wlev[k.level & 63], span + 7 * (int64_t)cm.s + 2 * cm.step[0] + 1);
+            wlev[k.level & 63] = std::max<int64_t>(wlev[k.level & 63], kDiagScale * (span + 7 * (int64_t)cm.s + 2 * cm.step[0] + 1));
         }
         auto order_by = [&](bool diag) {
             std::vector<Key> ks = keys;
