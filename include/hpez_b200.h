@@ -145,6 +145,10 @@ int hpez_plan_level_codes(hpez_plan plan, int64_t *out);
  * kernel's clock64 phase counters (grab, wait, work, units). */
 int hpez_plan_info(hpez_plan plan, int64_t *out);
 
+/* HPEZ_PROFILE plans only: per-level (first item start, last item end)
+ * globaltimer stamps of the flow kernel, 12 levels x 2 int64. */
+int hpez_plan_levels_timeline(hpez_plan plan, int64_t *out);
+
 /* Select the CUDA device for subsequent calls from this host thread. */
 int hpez_set_device(int32_t device);
 

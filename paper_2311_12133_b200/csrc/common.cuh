@@ -13,8 +13,11 @@
 
 namespace hpez {
 
+#ifndef HPEZ_ITEM_WARPS
+#define HPEZ_ITEM_WARPS 8
+#endif
 constexpr int kMaxRank = HPEZ_MAX_RANK;
-constexpr int kItemWarps = 8;              // warps per work item
+constexpr int kItemWarps = HPEZ_ITEM_WARPS;  // warps per work item
 constexpr int kItemThreads = kItemWarps * 32;
 
 // ------------------------------------------------------------ fast divmod --
@@ -132,33 +135,32 @@ __device__ __forceinline__ double round_native(double v) {
 // quant.quantize_block for one point (quant.py:80-105).  Returns the code;
 // *out is the decompressor-visible value (recon, or orig on escape).
 // The quotient x = (orig - pred) / (2e) is formed as a product with the
-// reciprocal; k = floor(|x| + 0.5) can only differ from the correctly rounded
-// division when |x| + 0.5 lies within a few ulps of an integer, in which case
-// the exact IEEE division decides.
+// reciprocal.  Its error is a few ulps of |x| + 0.5 (< 2^-30 absolute when
+// |x| + 0.5 < 2^20), so k = floor(|x| + 0.5) can only differ from the
+// correctly rounded division when the fraction lies within 2^-20 of an
+// integer, or when |x| + 0.5 >= 2^20 -- then the exact IEEE division decides.
 template <int ROUND>
-__device__ __forceinline__ int64_t quantize_point(double orig, double pred, double bound,
-                                                  double two_e, double inv_two_e, int64_t R,
-                                                  double *out) {
+__device__ __forceinline__ int32_t quantize_point(double orig, double pred, double bound, double two_e,
+                                                  double inv_two_e, double Rd, int32_t R, double *out) {
     double recon;
     bool ok;
-    int64_t code;
+    int32_t code;
     if (bound > 0.0) {
         const double d = __dsub_rn(orig, pred);
         double x = __dmul_rn(d, inv_two_e);
-        double y = __dadd_rn(fabs(x), 0.5);
+        const double y = __dadd_rn(fabs(x), 0.5);
         double fl = floor(y);
         const double fr = __dsub_rn(y, fl);
-        const double margin = __dmul_rn(y, 0x1p-40);
-        if (fr < margin || fr > __dsub_rn(1.0, margin)) {
+        if (fr < 0x1p-20 || fr > 1.0 - 0x1p-20 || y >= 0x1p20) {
             x = __ddiv_rn(d, two_e);
             fl = floor(__dadd_rn(fabs(x), 0.5));
         }
         double k = x > 0.0 ? fl : (x < 0.0 ? -fl : 0.0);  // np.sign(x) * fl
-        const bool inr = fabs(k) < (double)R;
+        const bool inr = fabs(k) < Rd;
         if (!inr) k = 0.0;
         recon = round_native<ROUND>(__dadd_rn(pred, __dmul_rn(two_e, k)));
         ok = inr && (fabs(__dsub_rn(recon, orig)) <= bound);
-        code = ok ? (int64_t)k + R : 0;
+        code = ok ? (int32_t)k + R : 0;
     } else {
         recon = round_native<ROUND>(pred);
         ok = recon == orig;
@@ -166,6 +168,13 @@ __device__ __forceinline__ int64_t quantize_point(double orig, double pred, doub
     }
     *out = ok ? recon : orig;
     return code;
+}
+
+// 64-bit-radius-free wrapper kept for the generic path
+template <int ROUND>
+__device__ __forceinline__ int64_t quantize_point(double orig, double pred, double bound, double two_e,
+                                                  double inv_two_e, int64_t R, double *out) {
+    return quantize_point<ROUND>(orig, pred, bound, two_e, inv_two_e, (double)R, (int32_t)R, out);
 }
 
 // quant.dequantize_block for a non-escape code (quant.py:115-121).

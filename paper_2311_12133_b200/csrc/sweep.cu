@@ -31,6 +31,13 @@
 
 #include "common.cuh"
 
+#ifndef HPEZ_L1_PREFETCH
+#define HPEZ_L1_PREFETCH 0  // measured slower on B200 (kept for experiments)
+#endif
+#ifndef HPEZ_FLOW_OCC
+#define HPEZ_FLOW_OCC 4  // flow-kernel CTAs per SM the fast path is compiled for
+#endif
+
 namespace hpez {
 
 __constant__ RowEntry c_rows[kFamilies][64];
@@ -260,6 +267,7 @@ struct SweepArgs {
     const int32_t *coarse_groups; // [g0, g1) pair ranges, one per (level, depth)
     int32_t n_groups;
     unsigned long long *prof;   // optional phase counters (HPEZ_PROFILE)
+    int32_t dbg;                // HPEZ_DEBUG_NODEPS timing experiments only
     const int64_t *wbase;       // per (item, warp): code index of the first member
     const int32_t *wn;          // per (item, warp): member count
     uint32_t *esc_cnt;          // per (item, warp): escapes (compress, written)
@@ -470,6 +478,61 @@ __device__ __forceinline__ double p1d(const T *__restrict__ w, int idx, int c, i
     return DA(DM(-1.0, v(-2)), DM(2.0, v(-1)));
 }
 
+// Stencil families at compile time: nominal offsets, interior test and the
+// full-row combination in the reference's left-to-right order.
+template <int FAM> struct Fam;
+template <> struct Fam<FAM_LIN_I> {
+    static constexpr int n = 2;
+    __device__ static constexpr int u(int i) { return i == 0 ? -1 : 1; }
+    __device__ static bool interior(int c, int E, int s) { return c + s <= E - 1; }
+    template <typename V> __device__ static double combine(const V (&v)[6]) {
+        return DA(DM(0.5, (double)v[0]), DM(0.5, (double)v[1]));
+    }
+};
+template <> struct Fam<FAM_NAK_I> {
+    static constexpr int n = 4;
+    __device__ static constexpr int u(int i) { return i == 0 ? -3 : i == 1 ? -1 : i == 2 ? 1 : 3; }
+    __device__ static bool interior(int c, int E, int s) { return c >= 3 * s && c + 3 * s <= E - 1; }
+    template <typename V> __device__ static double combine(const V (&v)[6]) {
+        return DA(DA(DA(DM(-1.0 / 16, (double)v[0]), DM(9.0 / 16, (double)v[1])), DM(9.0 / 16, (double)v[2])),
+                  DM(-1.0 / 16, (double)v[3]));
+    }
+};
+template <> struct Fam<FAM_NAT_I> {
+    static constexpr int n = 4;
+    __device__ static constexpr int u(int i) { return i == 0 ? -3 : i == 1 ? -1 : i == 2 ? 1 : 3; }
+    __device__ static bool interior(int c, int E, int s) { return c >= 3 * s && c + 3 * s <= E - 1; }
+    template <typename V> __device__ static double combine(const V (&v)[6]) {
+        return DA(DA(DA(DM(-3.0 / 40, (double)v[0]), DM(23.0 / 40, (double)v[1])), DM(23.0 / 40, (double)v[2])),
+                  DM(-3.0 / 40, (double)v[3]));
+    }
+};
+template <> struct Fam<FAM_NAK_S> {
+    static constexpr int n = 4;
+    __device__ static constexpr int u(int i) { return i == 0 ? -2 : i == 1 ? -1 : i == 2 ? 1 : 2; }
+    __device__ static bool interior(int c, int E, int s) { return c + 2 * s <= E - 1; }
+    template <typename V> __device__ static double combine(const V (&v)[6]) {
+        return DA(DA(DA(DM(-1.0 / 6, (double)v[0]), DM(4.0 / 6, (double)v[1])), DM(4.0 / 6, (double)v[2])),
+                  DM(-1.0 / 6, (double)v[3]));
+    }
+};
+template <> struct Fam<FAM_NAT_S> {
+    static constexpr int n = 6;
+    __device__ static constexpr int u(int i) {
+        return i == 0 ? -3 : i == 1 ? -2 : i == 2 ? -1 : i == 3 ? 1 : i == 4 ? 2 : 3;
+    }
+    __device__ static bool interior(int c, int E, int s) { return c + 3 * s <= E - 1; }
+    template <typename V> __device__ static double combine(const V (&v)[6]) {
+        return DA(DA(DA(DA(DA(DM(3.0 / 62, (double)v[0]), DM(-18.0 / 62, (double)v[1])), DM(46.0 / 62, (double)v[2])),
+                        DM(46.0 / 62, (double)v[3])), DM(-18.0 / 62, (double)v[4])), DM(3.0 / 62, (double)v[5]));
+    }
+};
+
+// grid axis of blend term t for a fast-path layout KIND
+template <int KIND> __device__ constexpr int kind_axis(int t) {
+    return KIND < 3 ? KIND : KIND == 3 ? (t == 0 ? 0 : 1) : KIND == 4 ? (t == 0 ? 0 : 2) : KIND == 5 ? (t == 0 ? 1 : 2) : t;
+}
+
 template <typename T, typename C, int DIR, int ROUND, int KIND, int FAM>
 __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev &cm, int item, int warp) {
     const int lane = threadIdx.x & 31;
@@ -490,9 +553,12 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
     const double bound = cm.bound, two_e = cm.two_e, inv_two_e = cm.inv_two_e;
     const double w0 = cm.pred.w[0], w1 = cm.pred.w[1], w2 = cm.pred.w[2];
     const int64_t R = A.g.radius;
+    const int32_t R32 = (int32_t)R;
+    const double Rd = (double)R;
     T *__restrict__ work = (T *)A.work;
     C *__restrict__ codes = (C *)A.codes;
     const int64_t cb = cm.code_base;
+    C *__restrict__ cptr = codes + cb + p0 + lane;  // this lane's code slot, +32 per iteration
     const int64_t obase = DIR == HPEZ_DECOMPRESS ? A.esc_off[e] : 0;
     uint32_t nesc = 0;
     uint32_t p = p0 + lane;
@@ -505,35 +571,64 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
         const bool valid = pb + lane < pend;
         const int z = st0 + jz * sp0, y = st1 + jy * sp1, x = st2 + jx * sp2;
         const int idx = z * E0 + y * E1 + x;
-        const int64_t ci = cb + pb + lane;
         bool esc = false;
         if (valid) {
-            auto predict_fast = [&]() -> double {
-                if (KIND == 0) return p1d<FAM>(work, idx, z, D0, s, sE0);
-                if (KIND == 1) return p1d<FAM>(work, idx, y, D1, s, sE1);
-                if (KIND == 2) return p1d<FAM>(work, idx, x, D2, s, sE2);
-                if (KIND == 3) return DA(DM(w0, p1d<FAM>(work, idx, z, D0, s, sE0)), DM(w1, p1d<FAM>(work, idx, y, D1, s, sE1)));
-                if (KIND == 4) return DA(DM(w0, p1d<FAM>(work, idx, z, D0, s, sE0)), DM(w1, p1d<FAM>(work, idx, x, D2, s, sE2)));
-                if (KIND == 5) return DA(DM(w0, p1d<FAM>(work, idx, y, D1, s, sE1)), DM(w1, p1d<FAM>(work, idx, x, D2, s, sE2)));
-                return DA(DA(DM(w0, p1d<FAM>(work, idx, z, D0, s, sE0)), DM(w1, p1d<FAM>(work, idx, y, D1, s, sE1))),
-                          DM(w2, p1d<FAM>(work, idx, x, D2, s, sE2)));
-            };
-            if (DIR == HPEZ_COMPRESS) {
-                const double pred = predict_fast();
-                const double orig = ldv(work, idx);
-                double out;
-                const int64_t code = quantize_point<ROUND>(orig, pred, bound, two_e, inv_two_e, R, &out);
-                __stcg(codes + ci, (C)code);
-                esc = code == 0;
-                if (!esc) __stcg(work + idx, (T)out);
-            } else {
-                const int64_t code = (int64_t)codes[ci];
-                if (code != 0) {
-                    const double pred = predict_fast();
-                    __stcg(work + idx, (T)dequantize_point<ROUND>(pred, code, two_e, R));
-                } else {
-                    esc = true;
+            constexpr int NAX = KIND < 3 ? 1 : KIND < 6 ? 2 : 3;
+            const int crd[3] = {z, y, x};
+            const int Dv[3] = {D0, D1, D2};
+            const int sEv[3] = {sE0, sE1, sE2};
+            bool in_all = true;
+#pragma unroll
+            for (int t = 0; t < NAX; t++) {
+                const int a = kind_axis<KIND>(t);
+                in_all &= Fam<FAM>::interior(crd[a], Dv[a], s);
+            }
+            double pred;
+            double origv = 0.0;
+            int64_t code = 0;
+            if (in_all) {
+                // one memory round trip: every stencil value plus the original
+                // (compress) or the code (decompress) is requested up front
+                T v[NAX][6];
+                T o = T(0);
+                if (DIR == HPEZ_DECOMPRESS) code = (int64_t)*cptr;
+                else o = work[idx];
+#pragma unroll
+                for (int t = 0; t < NAX; t++) {
+                    const int a = kind_axis<KIND>(t);
+#pragma unroll
+                    for (int i = 0; i < Fam<FAM>::n; i++) v[t][i] = work[idx + Fam<FAM>::u(i) * sEv[a]];
                 }
+                double pt[NAX];
+#pragma unroll
+                for (int t = 0; t < NAX; t++) pt[t] = Fam<FAM>::combine(v[t]);
+                if (NAX == 1) pred = pt[0];
+                else if (NAX == 2) pred = DA(DM(w0, pt[0]), DM(w1, pt[NAX - 1]));
+                else pred = DA(DA(DM(w0, pt[0]), DM(w1, pt[1])), DM(w2, pt[NAX - 1]));
+                origv = (double)o;
+            } else {
+                if (DIR == HPEZ_DECOMPRESS) code = (int64_t)*cptr;
+                else origv = ldv(work, idx);
+                double pt[NAX];
+#pragma unroll
+                for (int t = 0; t < NAX; t++) {
+                    const int a = kind_axis<KIND>(t);
+                    pt[t] = p1d<FAM>(work, idx, crd[a], Dv[a], s, sEv[a]);
+                }
+                if (NAX == 1) pred = pt[0];
+                else if (NAX == 2) pred = DA(DM(w0, pt[0]), DM(w1, pt[NAX - 1]));
+                else pred = DA(DA(DM(w0, pt[0]), DM(w1, pt[1])), DM(w2, pt[NAX - 1]));
+            }
+            if (DIR == HPEZ_COMPRESS) {
+                double out;
+                const int32_t c = quantize_point<ROUND>(origv, pred, bound, two_e, inv_two_e, Rd, R32, &out);
+                *cptr = (C)c;
+                esc = c == 0;
+                if (!esc) work[idx] = (T)out;
+            } else if (code != 0) {
+                work[idx] = (T)dequantize_point<ROUND>(pred, code, two_e, R);
+            } else {
+                esc = true;
             }
         }
         const uint32_t eb = __ballot_sync(0xffffffffu, esc);
@@ -543,6 +638,7 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
             else atomicExch(A.flags, HPEZ_OUTLIER_UNDERFLOW);
         }
         nesc += __popc(eb);
+        cptr += 32;
         jx += 32;
         while (jx >= cn2) {
             jx -= cn2;
@@ -550,6 +646,26 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
                 jy = 0;
                 jz++;
             }
+        }
+        if (HPEZ_L1_PREFETCH && pb + 32 + lane < pend) {
+            // L1 prefetch of the next iteration's stencil lines (clamped in-grid)
+            constexpr int NAX = KIND < 3 ? 1 : KIND < 6 ? 2 : 3;
+            const int nz = st0 + jz * sp0, ny = st1 + jy * sp1, nx = st2 + jx * sp2;
+            const int nidx = nz * E0 + ny * E1 + nx;
+            const int sEv[3] = {sE0, sE1, sE2};
+            const int last = D0 * E0 - 1;
+#pragma unroll
+            for (int t = 0; t < NAX; t++) {
+                const int a = kind_axis<KIND>(t);
+#pragma unroll
+                for (int i = 0; i < Fam<FAM>::n; i++) {
+                    int q = nidx + Fam<FAM>::u(i) * sEv[a];
+                    q = q < 0 ? 0 : (q > last ? last : q);
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(work + q));
+                }
+            }
+            if (DIR == HPEZ_COMPRESS) asm volatile("prefetch.global.L1 [%0];" ::"l"(work + nidx));
+            else asm volatile("prefetch.global.L1 [%0];" ::"l"(cptr));
         }
     }
     if (DIR == HPEZ_COMPRESS && lane == 0) A.esc_cnt[e] = nesc;
@@ -604,20 +720,79 @@ __global__ void __launch_bounds__(1024) coarse_kernel(const __grid_constant__ Sw
     }
 }
 
+// TMA bulk prefetch into L2 of everything an item reads that no earlier
+// commit writes: its own originals (compress: one request per lattice row
+// segment) or its code range (decompress).  Issued by one warp, one item
+// ahead, so the DRAM latency overlaps the dependency wait and current work.
+__device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint64_t bytes) {
+    uint64_t a = (uint64_t)p & ~(uint64_t)15;
+    uint64_t e = ((uint64_t)p + bytes + 15) & ~(uint64_t)15;
+    while (a < e) {
+        const uint32_t n = (uint32_t)(e - a < (1ull << 20) ? e - a : (1ull << 20));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+        a += n;
+    }
+}
+
+template <typename T, typename C, int DIR>
+__device__ __forceinline__ void prefetch_item(const SweepArgs &A, int item, int lane) {
+    const CommitDev &cm = A.commits[A.item_commit[item]];
+    const int rank = A.g.rank;
+    const uint32_t P0 = (uint32_t)(item - cm.item_base) * (uint32_t)cm.p_item;
+    const uint32_t P1 = min(P0 + (uint32_t)cm.p_item, cm.npos);
+    if (DIR == HPEZ_DECOMPRESS) {
+        if (lane == 0 && cm.kind == COMMIT_UNIFORM)
+            bulk_prefetch_l2((const C *)A.codes + cm.code_base + P0, (uint64_t)(P1 - P0) * sizeof(C));
+        return;
+    }
+    const int x = rank - 1;
+    const uint32_t cx = (uint32_t)cm.cnt[x];
+    const uint32_t r0 = P0 / cx, r1 = (P1 - 1) / cx;
+    for (uint32_t r = r0 + lane; r <= r1; r += 32) {
+        uint32_t q = r;
+        int64_t base = 0;
+        for (int a = x - 1; a >= 0; a--) {
+            const uint32_t qq = a > 0 ? q / (uint32_t)cm.cnt[a] : 0u;
+            const int ja = (int)(q - qq * (uint32_t)cm.cnt[a]);
+            q = qq;
+            base += (int64_t)(cm.start[a] + ja * cm.step[a]) * A.g.estr[a];
+        }
+        const uint32_t xa = r == r0 ? P0 - r * cx : 0u;
+        const uint32_t xb = r == r1 ? P1 - 1 - r * cx : cx - 1;
+        const int64_t lo = base + cm.start[x] + (int64_t)xa * cm.step[x];
+        const int64_t hi = base + cm.start[x] + (int64_t)xb * cm.step[x];
+        bulk_prefetch_l2((const T *)A.work + lo, (uint64_t)(hi - lo + 1) * sizeof(T));
+    }
+}
+
 // Persistent dataflow kernel over the remaining items.
 template <typename T, typename C, int DIR, int ROUND, bool STATS, bool FAST>
-__global__ void __launch_bounds__(kItemThreads, FAST ? 4 : 3) flow_kernel(const __grid_constant__ SweepArgs A) {
+__global__ void __launch_bounds__(kItemThreads, FAST ? HPEZ_FLOW_OCC * 8 / kItemWarps : 3) flow_kernel(const __grid_constant__ SweepArgs A) {
     __shared__ CommitDev s_cm;
-    __shared__ int s_item;
+    __shared__ int s_item, s_next;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int cur = -1;
+    bool first = true;
     unsigned long long t_grab = 0, t_wait = 0, t_work = 0, n_done = 0;
+    int next_rel = 0;
+    if (threadIdx.x == 0) next_rel = atomicAdd(A.next, 1);
     while (true) {
         const long long c0 = A.prof ? clock64() : 0;
-        if (threadIdx.x == 0) s_item = atomicAdd(A.next, 1);
+        // the next item is claimed one step ahead, so the atomic's latency
+        // overlaps the previous item's work
+        if (threadIdx.x == 0) {
+            s_item = next_rel;
+            if (next_rel < A.n_items) next_rel = atomicAdd(A.next, 1);
+            s_next = next_rel;
+        }
         __syncthreads();
         const int rel = s_item;
         if (rel >= A.n_items) break;
+        if (warp == 1) {
+            if (first) prefetch_item<T, C, DIR>(A, A.flow_order[rel], lane);
+            if (s_next < A.n_items) prefetch_item<T, C, DIR>(A, A.flow_order[s_next], lane);
+        }
+        first = false;
         const int item = A.flow_order[rel];
         const int c = A.item_commit[item];
         if (c != cur) {
@@ -626,7 +801,7 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? 4 : 3) flow_kernel(const 
             cur = c;
         }
         const long long c1 = A.prof ? clock64() : 0;
-        if (warp == 0) {
+        if (warp == 0 && !A.dbg) {
             const int k0 = A.dep_off[item], k1 = A.dep_off[item + 1];
             for (int k = k0; k < k1; k++) {
                 const int2 d = A.dep_rng[k];
@@ -650,6 +825,13 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? 4 : 3) flow_kernel(const 
             t_wait += c2 - c1;
             t_work += c3 - c2;
             n_done++;
+            if (threadIdx.x == 0) {  // per-level first start / last end (globaltimer ns)
+                unsigned long long now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                const int lv = s_cm.level < 12 ? s_cm.level : 11;
+                atomicMin(A.prof + 8 + 2 * lv, now - (unsigned long long)((c3 - c2) / 1.9));
+                atomicMax(A.prof + 9 + 2 * lv, now);
+            }
         }
     }
     if (A.prof && threadIdx.x == 0) {
@@ -677,64 +859,71 @@ __global__ void __launch_bounds__(256) count_zero_kernel(const C *__restrict__ c
 }
 
 // Compress post-pass: outliers of every (item, warp) with escapes, in stream
-// order, read back from the grid (escaped points keep their originals).
+// order, read back from the grid (escaped points keep their originals).  One
+// warp screens 32 entries and replays only those that escaped.
 template <typename T, typename C>
 __global__ void __launch_bounds__(256) gather_outliers_kernel(const __grid_constant__ SweepArgs A, int64_t n_entries,
                                                               double *__restrict__ out, int64_t cap) {
-    const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t e0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
     const int lane = threadIdx.x & 31;
-    if (e >= n_entries || A.esc_cnt[e] == 0) return;
-    const int item = (int)(e / kItemWarps), warp = (int)(e % kItemWarps);
-    const CommitDev &cm = A.commits[A.item_commit[item]];
+    if (e0 >= n_entries) return;
+    const bool has = e0 + lane < n_entries && A.esc_cnt[e0 + lane] != 0;
+    uint32_t todo = __ballot_sync(0xffffffffu, has);
     const GridDev &g = A.g;
     const T *work = (const T *)A.work;
     const C *codes = (const C *)A.codes;
-    const uint32_t p0 = (uint32_t)(item - cm.item_base) * (uint32_t)cm.p_item + (uint32_t)warp * (uint32_t)cm.pw;
-    const uint32_t pend = min(p0 + (uint32_t)cm.pw, cm.npos);
-    int64_t cbase = A.wbase[e];
-    int64_t o = A.esc_off[e];
-    if (cm.kind == COMMIT_UNIFORM) {
-        // members are all positions: scan the warp's code range for escapes
-        const int n = (int)(pend - p0);
-        for (int k = 0; k < n; k += 32) {
-            const bool esc = k + lane < n && codes[cbase + k + lane] == 0;
+    while (todo) {
+        const int k = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const int64_t e = e0 + k;
+        const int item = (int)(e / kItemWarps), warp = (int)(e % kItemWarps);
+        const CommitDev &cm = A.commits[A.item_commit[item]];
+        const uint32_t p0 = (uint32_t)(item - cm.item_base) * (uint32_t)cm.p_item + (uint32_t)warp * (uint32_t)cm.pw;
+        const uint32_t pend = min(p0 + (uint32_t)cm.pw, cm.npos);
+        int64_t cbase = A.wbase[e];
+        int64_t o = A.esc_off[e];
+        if (cm.kind == COMMIT_UNIFORM) {
+            const int n = (int)(pend - p0);
+            for (int q = 0; q < n; q += 32) {
+                const bool esc = q + lane < n && codes[cbase + q + lane] == 0;
+                const uint32_t eb = __ballot_sync(0xffffffffu, esc);
+                if (esc) {
+                    int j[kMaxRank];
+                    decode_pos(cm, g.rank, p0 + q + lane, j);
+                    int64_t idx = 0;
+                    for (int a = 0; a < g.rank; a++) idx += (int64_t)(cm.start[a] + j[a] * cm.step[a]) * g.estr[a];
+                    const int64_t r = o + __popc(eb & ((1u << lane) - 1u));
+                    if (r < cap) out[r] = (double)work[idx];
+                }
+                o += __popc(eb);
+            }
+            continue;
+        }
+        for (uint32_t pb = p0; pb < pend; pb += 32) {
+            const uint32_t p = pb + lane;
+            const bool valid = p < pend;
+            int j[kMaxRank], coord[kMaxRank];
+            decode_pos(cm, g.rank, valid ? p : p0, j);
+            int64_t idx = 0;
+            uint32_t jodd = 0;
+            for (int a = 0; a < g.rank; a++) {
+                coord[a] = cm.start[a] + j[a] * cm.step[a];
+                idx += (int64_t)coord[a] * g.estr[a];
+                jodd |= (uint32_t)(j[a] & 1) << a;
+            }
+            bool member = valid;
+            if (valid) mixed_member(A, cm, coord, jodd, &member);
+            const uint32_t mb = __ballot_sync(0xffffffffu, member);
+            const int64_t ci = cbase + __popc(mb & ((1u << lane) - 1u));
+            const bool esc = member && codes[ci] == 0;
             const uint32_t eb = __ballot_sync(0xffffffffu, esc);
             if (esc) {
-                int j[kMaxRank];
-                decode_pos(cm, g.rank, p0 + k + lane, j);
-                int64_t idx = 0;
-                for (int a = 0; a < g.rank; a++) idx += (int64_t)(cm.start[a] + j[a] * cm.step[a]) * g.estr[a];
                 const int64_t r = o + __popc(eb & ((1u << lane) - 1u));
                 if (r < cap) out[r] = (double)work[idx];
             }
             o += __popc(eb);
+            cbase += __popc(mb);
         }
-        return;
-    }
-    for (uint32_t pb = p0; pb < pend; pb += 32) {
-        const uint32_t p = pb + lane;
-        const bool valid = p < pend;
-        int j[kMaxRank], coord[kMaxRank];
-        decode_pos(cm, g.rank, valid ? p : p0, j);
-        int64_t idx = 0;
-        uint32_t jodd = 0;
-        for (int a = 0; a < g.rank; a++) {
-            coord[a] = cm.start[a] + j[a] * cm.step[a];
-            idx += (int64_t)coord[a] * g.estr[a];
-            jodd |= (uint32_t)(j[a] & 1) << a;
-        }
-        bool member = valid;
-        if (valid) mixed_member(A, cm, coord, jodd, &member);
-        const uint32_t mb = __ballot_sync(0xffffffffu, member);
-        const int64_t ci = cbase + __popc(mb & ((1u << lane) - 1u));
-        const bool esc = member && codes[ci] == 0;
-        const uint32_t eb = __ballot_sync(0xffffffffu, esc);
-        if (esc) {
-            const int64_t r = o + __popc(eb & ((1u << lane) - 1u));
-            if (r < cap) out[r] = (double)work[idx];
-        }
-        o += __popc(eb);
-        cbase += __popc(mb);
     }
 }
 
@@ -990,7 +1179,7 @@ static int num_sms() {
 }
 
 constexpr uint32_t kCoarseMax = 512;  // leading levels whose commits are all this small run in the coarse CTA
-static int kDiagScale = 2;  // commits at most this large run in the coarse CTA
+static int kDiagScale = 8;  // commits at most this large run in the coarse CTA
 
 struct Plan {
     hpez_sweep_desc d{};
@@ -1390,7 +1579,7 @@ struct Plan {
     void build_items() {
         const int sms = num_sms();
         if (const char *ev = getenv("HPEZ_DIAG_SCALE")) kDiagScale = std::max(1, atoi(ev));
-        int pmax = 4096;
+        int pmax = 512 * kItemWarps;
         if (const char *ev = getenv("HPEZ_ITEM_MAX")) pmax = std::max(256, atoi(ev));
         uint32_t coarse_max = kCoarseMax;
         if (const char *ev = getenv("HPEZ_COARSE_MAX")) coarse_max = (uint32_t)atoi(ev);
@@ -1646,6 +1835,7 @@ static SweepArgs base_args(Plan &p) {
     A.coarse_groups = p.d_coarse_groups;
     A.n_groups = (int32_t)(p.coarse_groups.size() / 2);
     A.prof = p.d_prof;
+    A.dbg = getenv("HPEZ_DEBUG_NODEPS") ? 1 : 0;
     A.wbase = p.d_wbase;
     A.wn = p.d_wn;
     A.esc_cnt = p.d_esc_cnt;
@@ -1684,8 +1874,10 @@ static int plan_setup(Plan *p, cudaStream_t st) {
     if (!e) e = dupload(&p->d_table, p->table);
     if (!e) e = dupload(&p->d_mixed_items, p->mixed_items);
     if (!e && getenv("HPEZ_PROFILE")) {
-        e = dalloc(&p->d_prof, 8);
+        e = dalloc(&p->d_prof, 32);
         if (!e) e = cudaMemset(p->d_prof, 0, 8 * sizeof(unsigned long long));
+        if (!e) e = cudaMemset(p->d_prof + 8, 0xff, 24 * sizeof(unsigned long long));
+        for (int l = 0; l < 12 && !e; l++) e = cudaMemset(p->d_prof + 9 + 2 * l, 0, sizeof(unsigned long long));
     }
     const size_t nc = std::max<size_t>(p->commits.size(), 1);
     std::vector<int32_t> clevel(nc, 0);
@@ -1770,6 +1962,14 @@ int32_t hpez_plan_num_launches(hpez_plan plan) {
 // diag_order, flow_fast, coarse_fast, dep_intervals] and, when the plan was
 // built with HPEZ_PROFILE set, the flow kernel's accumulated clock64 phase
 // counters [grab, wait, work, items] (out[8..11]).
+int hpez_plan_levels_timeline(hpez_plan plan, int64_t *out) {  // 24 values (start, end) x 12 levels
+    if (!plan || !out || !plan->p.d_prof) return HPEZ_BAD_ARGUMENT;
+    unsigned long long h[24];
+    if (cudaMemcpy(h, plan->p.d_prof + 8, sizeof h, cudaMemcpyDeviceToHost) != cudaSuccess) return HPEZ_CUDA_ERROR;
+    for (int i = 0; i < 24; i++) out[i] = (int64_t)h[i];
+    return HPEZ_OK;
+}
+
 int hpez_plan_info(hpez_plan plan, int64_t *out) {
     if (!plan || !out) return HPEZ_BAD_ARGUMENT;
     const Plan &p = plan->p;
@@ -1858,7 +2058,7 @@ int hpez_sweep_run(hpez_plan plan, void *work, void *codes, int64_t codes_avail,
     if (e) return cuda_status(e);
     if (p.d.direction == HPEZ_COMPRESS) {
         exclusive_scan(p.d_esc_cnt, ne, p.d_esc_off, p.d_scan_tmp, p.d_total, st);
-        const int64_t thr = ne * 32;
+        const int64_t thr = (ne + 31) / 32 * 32;
         auto *gk = p.d.work_dtype == HPEZ_WORK_F32
                        ? (p.d.code_dtype == HPEZ_CODES_U16 ? gather_outliers_kernel<float, uint16_t>
                                                            : gather_outliers_kernel<float, int32_t>)
