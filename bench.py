@@ -72,52 +72,58 @@ def md_weights_for(field):
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """NVML sampler (background thread, ~1 kHz) running during the timed region:
+    SM clock, max SM clock and the active clock-event (throttle) reasons."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index):
-        self.index = index
-        self.p = None
+    def __init__(self, cuda_index):
+        self.cuda_index = cuda_index
+        self.samples, self.reasons, self.max = [], set(), None
+        self._stop = False
+        self._t = None
+
+    def _run(self, h, nv):
+        while not self._stop:
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                break
+            time.sleep(0.001)
 
     def __enter__(self):
         try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import threading
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            bus = torch.cuda.get_device_properties(self.cuda_index).pci_bus_id
+            try:
+                h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = nv.nvmlDeviceGetHandleByIndex(self.cuda_index)
+            self.max = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, args=(h, nv), daemon=True)
+            self._t.start()
+            time.sleep(0.003)
         except Exception:
-            self.p = None
+            self._t = None
         return self
 
     def __exit__(self, *a):
-        self.out = ""
-        if self.p is not None:
-            self.p.terminate()
-            try:
-                self.out, _ = self.p.communicate(timeout=5)
-            except Exception:
-                self.p.kill()
+        self._stop = True
+        if self._t is not None:
+            self._t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in (self.out or "").strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, f[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max, "samples": len(self.samples),
+                "reasons": sorted(self.reasons), "source": "nvml"}
 
 
 def dist_setup(n_gpus):
@@ -274,6 +280,7 @@ def run_b200(args):
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get("compress_dram_bytes_per_sweep")
+            traffic = None if traffic is None else round(traffic / (tc_mean / 1e3) / 1e9, 1)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
@@ -287,7 +294,9 @@ def run_b200(args):
                        "achieved_gbs": round(ach_d, 1), "frac": round(ach_d / peak, 4)},
         "roofline": {"bound": "hbm", "achieved": round(ach_c, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(ach_c / peak, 4), "traffic": traffic,
-                     "kernel": "compress sweep (commit_kernel launches of one run_levels)",
+                     "traffic_note": "ncu dram__bytes_read+write of one compress sweep "
+                                     "(profiles/traffic_cfg2.json) over this run's sweep time, GB/s",
+                     "kernel": "compress sweep (coarse + flow + escape scan/gather kernels of one run_levels)",
                      "algorithmic_bytes": f"{BYTES_COMPRESS} B/pt x {n} pts",
                      "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"},
         "e2e": {"value": round(world * gb / (e2e_ms / 1e3), 3), "unit": UNIT,

@@ -123,6 +123,12 @@ struct CommitDev {
     PredDev pred;               // uniform commits
 };
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // ------------------------------------------------------------- quantizer --
 template <int ROUND>
 __device__ __forceinline__ double round_native(double v) {

@@ -265,9 +265,11 @@ struct SweepArgs {
     const int2 *dep_rng;          // item-id intervals (inclusive)
     const int32_t *coarse_pairs;  // (commit, item) pairs of the coarse prefix
     const int32_t *coarse_groups; // [g0, g1) pair ranges, one per (level, depth)
+    int32_t n_coarse_commits;     // commit descriptors [0, n) staged in the coarse kernel's smem
     int32_t n_groups;
     unsigned long long *prof;   // optional phase counters (HPEZ_PROFILE)
     int32_t dbg;                // HPEZ_DEBUG_NODEPS timing experiments only
+    int32_t l2_prefetch;        // TMA bulk L2 prefetch of the next item (HPEZ_L2_PREFETCH=1)
     const int64_t *wbase;       // per (item, warp): code index of the first member
     const int32_t *wn;          // per (item, warp): member count
     uint32_t *esc_cnt;          // per (item, warp): escapes (compress, written)
@@ -692,32 +694,48 @@ __device__ __forceinline__ void process_dispatch(const SweepArgs &A, const Commi
 #undef HPEZ_FAST
 }
 
-// Leading tiny levels: one CTA of 4 groups x 8 warps.  All commits of one
-// (level, DAG depth) group are independent and run concurrently; groups are
-// separated by __syncthreads.
-__device__ __forceinline__ void group_bar(int id) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kItemThreads) : "memory");
+// Leading small levels on one thread-block cluster (up to 16 CTAs x 1024
+// threads, one per SM).  Every coarse commit descriptor sits in shared
+// memory; the commits of one (level, DAG depth) group are independent, so
+// their (item, warp) units are spread over all warps of the cluster, and
+// groups are separated by a cluster barrier.  Its release/acquire form
+// orders the grid writes at GPU scope and invalidates L1 on the wait side,
+// so the plain L1-cached stencil loads of the next group see them.
+constexpr int kCoarseThreads = 1024;
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 template <typename T, typename C, int DIR, int ROUND, bool STATS, bool FAST>
-__global__ void __launch_bounds__(1024) coarse_kernel(const __grid_constant__ SweepArgs A) {
-    __shared__ CommitDev s_cm[4];
-    const int group = threadIdx.x / kItemThreads;
-    const int gt = threadIdx.x % kItemThreads;
-    const int warp = gt >> 5;
+__global__ void __launch_bounds__(kCoarseThreads, 1) coarse_kernel(const __grid_constant__ SweepArgs A) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    CommitDev *s_cm = reinterpret_cast<CommitDev *>(s_raw);
+    const int n_words = A.n_coarse_commits * (int)(sizeof(CommitDev) / 4);
+    for (int i = threadIdx.x; i < n_words; i += blockDim.x)
+        ((uint32_t *)s_cm)[i] = ((const uint32_t *)A.commits)[i];
+    __syncthreads();
+    const int nwarps = (int)(gridDim.x * blockDim.x) >> 5;
+    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const bool tprof = A.prof && blockIdx.x == 0 && threadIdx.x == 0;
+    const unsigned long long tg0 = tprof ? globaltimer() : 0;
     for (int g = 0; g < A.n_groups; g++) {
         const int t0 = A.coarse_groups[2 * g], t1 = A.coarse_groups[2 * g + 1];
-        for (int t = t0 + group; t < t1; t += 4) {
+        for (int rep = 0; rep < (A.dbg >> 4) + 1; rep++) {
+        for (int u = gw; u < ((A.dbg & 2) ? 0 : (t1 - t0) * kItemWarps); u += nwarps) {
+            const int t = t0 + u / kItemWarps;
             const int c = A.coarse_pairs[2 * t], item = A.coarse_pairs[2 * t + 1];
-            if (gt < sizeof(CommitDev) / 4)
-                ((uint32_t *)&s_cm[group])[gt] = ((const uint32_t *)&A.commits[c])[gt];
-            group_bar(group + 1);
-            if (FAST) process_dispatch<T, C, DIR, ROUND>(A, s_cm[group], item, warp);
-            else process_warp<T, C, DIR, ROUND, STATS>(A, s_cm[group], item, warp);
-            group_bar(group + 1);
+            if (FAST) process_dispatch<T, C, DIR, ROUND>(A, s_cm[c], item, u % kItemWarps);
+            else process_warp<T, C, DIR, ROUND, STATS>(A, s_cm[c], item, u % kItemWarps);
         }
-        __syncthreads();
+        cluster_sync_all();
+        if (tprof && g < 32) A.prof[32 + 2 * g + rep] = globaltimer() - tg0;
+        }
     }
+    if (tprof)
+        for (int g = 0; g < A.n_groups && g < 32; g++)
+            printf("coarse group %d: pairs %d, t=%.2f %.2f us\n", g, A.coarse_groups[2 * g + 1] - A.coarse_groups[2 * g],
+                   A.prof[32 + 2 * g] * 1e-3, A.prof[33 + 2 * g] * 1e-3);
 }
 
 // TMA bulk prefetch into L2 of everything an item reads that no earlier
@@ -788,7 +806,7 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? HPEZ_FLOW_OCC * 8 / kItem
         __syncthreads();
         const int rel = s_item;
         if (rel >= A.n_items) break;
-        if (warp == 1) {
+        if (warp == 1 && A.l2_prefetch) {
             if (first) prefetch_item<T, C, DIR>(A, A.flow_order[rel], lane);
             if (s_next < A.n_items) prefetch_item<T, C, DIR>(A, A.flow_order[s_next], lane);
         }
@@ -801,7 +819,7 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? HPEZ_FLOW_OCC * 8 / kItem
             cur = c;
         }
         const long long c1 = A.prof ? clock64() : 0;
-        if (warp == 0 && !A.dbg) {
+        if (warp == 0 && !(A.dbg & 1)) {
             const int k0 = A.dep_off[item], k1 = A.dep_off[item + 1];
             for (int k = k0; k < k1; k++) {
                 const int2 d = A.dep_rng[k];
@@ -1178,8 +1196,9 @@ static int num_sms() {
     return sms;
 }
 
-constexpr uint32_t kCoarseMax = 512;  // leading levels whose commits are all this small run in the coarse CTA
-static int kDiagScale = 8;  // commits at most this large run in the coarse CTA
+constexpr uint32_t kCoarseMax = 12000;  // leading levels of at most this many points (cumulative) run on the coarse cluster
+constexpr int kCoarseCluster = 16;
+static int kDiagScale = 8;  // diagonal order: item window width, in units of the dependency reach
 
 struct Plan {
     hpez_sweep_desc d{};
@@ -1198,6 +1217,7 @@ struct Plan {
     std::vector<int64_t> level_codes;
     int32_t n_items = 0;
     int32_t c_coarse = 0;      // commits [0, c_coarse) run in the coarse kernel
+    int32_t coarse_cluster = kCoarseCluster;  // CTAs in the coarse cluster
     bool coarse_fast = false, flow_fast = false, diag_order = false;
     int32_t first_flow_item = 0;
     std::vector<int32_t> item_commit;
@@ -1583,12 +1603,27 @@ struct Plan {
         if (const char *ev = getenv("HPEZ_ITEM_MAX")) pmax = std::max(256, atoi(ev));
         uint32_t coarse_max = kCoarseMax;
         if (const char *ev = getenv("HPEZ_COARSE_MAX")) coarse_max = (uint32_t)atoi(ev);
+        if (const char *ev = getenv("HPEZ_COARSE_CLUSTER")) coarse_cluster = std::max(1, std::min(16, atoi(ev)));
         const int nc = (int)commits.size();
+        // coarse prefix: leading levels of at most coarse_max points (latency-bound)
+        c_coarse = 0;
+        {
+            int c = 0;
+            uint64_t pts = 0;
+            while (c < nc) {
+                int e = c;
+                while (e < nc && commits[e].level == commits[c].level) pts += commits[e++].npos;
+                if (pts > coarse_max || (size_t)e * sizeof(CommitDev) > 200 * 1024) break;
+                c = e;
+            }
+            c_coarse = c;
+        }
         int32_t item = 0;
         for (int ci = 0; ci < nc; ci++) {
             CommitDev &cm = commits[ci];
             int64_t p = (int64_t)cm.npos / (4 * sms);
-            p = std::max<int64_t>(256, std::min<int64_t>(pmax, p));
+            // coarse commits: one position per lane, so a warp unit is one round trip
+            p = ci < c_coarse ? 256 : std::max<int64_t>(256, std::min<int64_t>(pmax, p));
             p = (p + 255) / 256 * 256;
             cm.p_item = (int32_t)p;
             cm.pw = (int32_t)(p / kItemWarps);
@@ -1628,19 +1663,6 @@ struct Plan {
             for (int c = lv_begin; c < lv_end; c++)
                 if (!has_succ[c]) prev_sinks.push_back(c);
             lv_begin = lv_end;
-        }
-        // coarse prefix: leading levels whose commits are all tiny
-        c_coarse = 0;
-        {
-            int c = 0;
-            while (c < nc) {
-                int e = c;
-                bool tiny = true;
-                while (e < nc && commits[e].level == commits[c].level) tiny &= commits[e++].npos <= coarse_max;
-                if (!tiny) break;
-                c = e;
-            }
-            c_coarse = c;
         }
         // coarse schedule: (level, depth) groups of (commit, item) pairs
         coarse_pairs.clear();
@@ -1748,6 +1770,7 @@ struct Plan {
             bool &f = ci < c_coarse ? coarse_fast : flow_fast;
             f = f && cm.fast_id >= 0;
         }
+        if (getenv("HPEZ_COARSE_GENERIC")) coarse_fast = false;
     }
     int d_rank() const { return d.rank; }
 };
@@ -1835,7 +1858,8 @@ static SweepArgs base_args(Plan &p) {
     A.coarse_groups = p.d_coarse_groups;
     A.n_groups = (int32_t)(p.coarse_groups.size() / 2);
     A.prof = p.d_prof;
-    A.dbg = getenv("HPEZ_DEBUG_NODEPS") ? 1 : 0;
+    A.dbg = (getenv("HPEZ_DEBUG_NODEPS") ? 1 : 0) | (getenv("HPEZ_COARSE_REPEAT") ? 16 : 0) | (getenv("HPEZ_COARSE_SKIP") ? 2 : 0);
+    A.l2_prefetch = getenv("HPEZ_L2_PREFETCH") ? atoi(getenv("HPEZ_L2_PREFETCH")) : 0;
     A.wbase = p.d_wbase;
     A.wn = p.d_wn;
     A.esc_cnt = p.d_esc_cnt;
@@ -1874,7 +1898,7 @@ static int plan_setup(Plan *p, cudaStream_t st) {
     if (!e) e = dupload(&p->d_table, p->table);
     if (!e) e = dupload(&p->d_mixed_items, p->mixed_items);
     if (!e && getenv("HPEZ_PROFILE")) {
-        e = dalloc(&p->d_prof, 32);
+        e = dalloc(&p->d_prof, 96);
         if (!e) e = cudaMemset(p->d_prof, 0, 8 * sizeof(unsigned long long));
         if (!e) e = cudaMemset(p->d_prof + 8, 0xff, 24 * sizeof(unsigned long long));
         for (int l = 0; l < 12 && !e; l++) e = cudaMemset(p->d_prof + 9 + 2 * l, 0, sizeof(unsigned long long));
@@ -2044,7 +2068,28 @@ int hpez_sweep_run(hpez_plan plan, void *work, void *codes, int64_t codes_avail,
     }
     if (!p.coarse_groups.empty()) {
         sweep_fn f = (p.coarse_fast && ks.coarse_fast) ? ks.coarse_fast : ks.coarse;
-        f<<<1, 1024, 0, st>>>(A);
+        const size_t smem = (size_t)p.c_coarse * sizeof(CommitDev);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1));
+        cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        A.n_coarse_commits = p.c_coarse;
+        cudaError_t le = cudaErrorUnknown;
+        for (int cl = p.coarse_cluster; cl >= 1 && le != cudaSuccess; cl /= 2) {
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(cl);
+            lc.blockDim = dim3(kCoarseThreads);
+            lc.dynamicSmemBytes = smem;
+            lc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            le = cudaLaunchKernelEx(&lc, f, A);
+            if (le != cudaSuccess) cudaGetLastError();  // cluster too large here: halve it
+        }
+        if (le != cudaSuccess) return cuda_status(le);
     }
     if (!p.flow_order.empty()) {
         A.n_items = (int32_t)p.flow_order.size();
