@@ -145,8 +145,9 @@ int hpez_plan_level_codes(hpez_plan plan, int64_t *out);
  * kernel's clock64 phase counters (grab, wait, work, units). */
 int hpez_plan_info(hpez_plan plan, int64_t *out);
 
-/* HPEZ_PROFILE plans only: per-level (first item start, last item end)
- * globaltimer stamps of the flow kernel, 12 levels x 2 int64. */
+/* HPEZ_PROFILE plans only: out[0..24) per-level (first item start, last
+ * item end) globaltimer stamps of the flow kernel, 12 levels x 2; out[24..72)
+ * per-level accumulated (grab, wait, work) SM cycles and item count, 12 x 4. */
 int hpez_plan_levels_timeline(hpez_plan plan, int64_t *out);
 
 /* Select the CUDA device for subsequent calls from this host thread. */

@@ -443,41 +443,40 @@ __device__ __forceinline__ void process_warp(const SweepArgs &A, const CommitDev
 // written out: inter-level cubic rows try (-1,1,3), (-3,-1,1), (-1,1),
 // (-3,-1), (-1,); same-level rows (-2,-1,1,2), (-2,-1,1), (-2,-1); a
 // truncated 6-point natural row falls back to the 4-point not-a-knot row.
-template <int FAM, typename T>
-__device__ __forceinline__ double p1d(const T *__restrict__ w, int idx, int c, int E, int s, int sE) {
-    auto v = [&](int u) { return (double)w[idx + u * sE]; };
+// Edge rows of family FAM at coordinate c (extent E, stride s) over values
+// x[] already loaded at the family's nominal offsets (Fam<FAM>::u order),
+// with every truncation of kernels.resolve_row (kernels.py:106-150) written
+// out: inter-level cubic rows try (-1,1,3), (-3,-1,1), (-1,1), (-3,-1),
+// (-1,); same-level rows (-2,-1,1,2), (-2,-1,1), (-2,-1); a truncated
+// 6-point natural row falls back to the 4-point not-a-knot row.  Offsets
+// outside the grid were loaded from the target itself and are never used.
+template <int FAM>
+__device__ __forceinline__ double edge_row(const double (&x)[6], int c, int E, int s) {
     const bool r1 = c + s <= E - 1;
-    if (FAM == FAM_LIN_I) {
-        if (r1) return DA(DM(0.5, v(-1)), DM(0.5, v(1)));
-        return DM(1.0, v(-1));
-    }
+    if (FAM == FAM_LIN_I) return r1 ? DA(DM(0.5, x[0]), DM(0.5, x[1])) : DM(1.0, x[0]);
     if (FAM == FAM_NAK_I || FAM == FAM_NAT_I) {
+        const double a = x[0], b = x[1], d = x[2], e = x[3];
         const bool l3 = c >= 3 * s, r3 = c + 3 * s <= E - 1;
         if (l3 && r3) {
-            const double a = v(-3), b = v(-1), d = v(1), e = v(3);
             if (FAM == FAM_NAK_I)
                 return DA(DA(DA(DM(-1.0 / 16, a), DM(9.0 / 16, b)), DM(9.0 / 16, d)), DM(-1.0 / 16, e));
             return DA(DA(DA(DM(-3.0 / 40, a), DM(23.0 / 40, b)), DM(23.0 / 40, d)), DM(-3.0 / 40, e));
         }
-        if (r3) return DA(DA(DM(3.0 / 8, v(-1)), DM(3.0 / 4, v(1))), DM(-1.0 / 8, v(3)));
-        if (l3 && r1) return DA(DA(DM(-1.0 / 8, v(-3)), DM(3.0 / 4, v(-1))), DM(3.0 / 8, v(1)));
-        if (r1) return DA(DM(0.5, v(-1)), DM(0.5, v(1)));
-        if (l3) return DA(DM(-0.5, v(-3)), DM(1.5, v(-1)));
-        return DM(1.0, v(-1));
+        if (r3) return DA(DA(DM(3.0 / 8, b), DM(3.0 / 4, d)), DM(-1.0 / 8, e));
+        if (l3 && r1) return DA(DA(DM(-1.0 / 8, a), DM(3.0 / 4, b)), DM(3.0 / 8, d));
+        if (r1) return DA(DM(0.5, b), DM(0.5, d));
+        if (l3) return DA(DM(-0.5, a), DM(1.5, b));
+        return DM(1.0, b);
     }
     // same-level families: targets sit at >= 3s, so only the right side truncates
-    const bool r2 = c + 2 * s <= E - 1;
-    if (FAM == FAM_NAT_S && c + 3 * s <= E - 1) {
-        const double a = v(-3), b = v(-2), d = v(-1), e = v(1), f = v(2), h = v(3);
-        return DA(DA(DA(DA(DA(DM(3.0 / 62, a), DM(-18.0 / 62, b)), DM(46.0 / 62, d)), DM(46.0 / 62, e)),
-                     DM(-18.0 / 62, f)), DM(3.0 / 62, h));
-    }
-    if (r2) {
-        const double a = v(-2), b = v(-1), d = v(1), e = v(2);
-        return DA(DA(DA(DM(-1.0 / 6, a), DM(4.0 / 6, b)), DM(4.0 / 6, d)), DM(-1.0 / 6, e));
-    }
-    if (r1) return DA(DA(DM(-1.0 / 3, v(-2)), DM(1.0, v(-1))), DM(1.0 / 3, v(1)));
-    return DA(DM(-1.0, v(-2)), DM(2.0, v(-1)));
+    constexpr int o = FAM == FAM_NAT_S ? 1 : 0;
+    const double b = x[o], d = x[o + 1], e = x[o + 2], f = x[o + 3];
+    if (FAM == FAM_NAT_S && c + 3 * s <= E - 1)
+        return DA(DA(DA(DA(DA(DM(3.0 / 62, x[0]), DM(-18.0 / 62, b)), DM(46.0 / 62, d)), DM(46.0 / 62, e)),
+                     DM(-18.0 / 62, f)), DM(3.0 / 62, x[5]));
+    if (c + 2 * s <= E - 1) return DA(DA(DA(DM(-1.0 / 6, b), DM(4.0 / 6, d)), DM(4.0 / 6, e)), DM(-1.0 / 6, f));
+    if (r1) return DA(DA(DM(-1.0 / 3, b), DM(1.0, d)), DM(1.0 / 3, e));
+    return DA(DM(-1.0, b), DM(2.0, d));
 }
 
 // Stencil families at compile time: nominal offsets, interior test and the
@@ -574,53 +573,65 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
         const int z = st0 + jz * sp0, y = st1 + jy * sp1, x = st2 + jx * sp2;
         const int idx = z * E0 + y * E1 + x;
         bool esc = false;
-        if (valid) {
-            constexpr int NAX = KIND < 3 ? 1 : KIND < 6 ? 2 : 3;
-            const int crd[3] = {z, y, x};
-            const int Dv[3] = {D0, D1, D2};
-            const int sEv[3] = {sE0, sE1, sE2};
-            bool in_all = true;
+        constexpr int NAX = KIND < 3 ? 1 : KIND < 6 ? 2 : 3;
+        const int crd[3] = {z, y, x};
+        const int Dv[3] = {D0, D1, D2};
+        const int sEv[3] = {sE0, sE1, sE2};
+        bool in_all = true;
 #pragma unroll
-            for (int t = 0; t < NAX; t++) {
-                const int a = kind_axis<KIND>(t);
-                in_all &= Fam<FAM>::interior(crd[a], Dv[a], s);
-            }
+        for (int t = 0; t < NAX; t++) {
+            const int a = kind_axis<KIND>(t);
+            in_all &= Fam<FAM>::interior(crd[a], Dv[a], s);
+        }
+        // warp-uniform split: a warp with any edge lane loads every lane's
+        // stencil with in-grid (clamped) addresses, so it still costs a single
+        // memory round trip; only the row arithmetic differs per lane
+        const bool warp_interior = __all_sync(0xffffffffu, in_all || !valid);
+        if (valid) {
             double pred;
             double origv = 0.0;
             int64_t code = 0;
-            if (in_all) {
-                // one memory round trip: every stencil value plus the original
-                // (compress) or the code (decompress) is requested up front
-                T v[NAX][6];
-                T o = T(0);
-                if (DIR == HPEZ_DECOMPRESS) code = (int64_t)*cptr;
-                else o = work[idx];
+            // one memory round trip: every stencil value plus the original
+            // (compress) or the code (decompress) is requested up front
+            T v[NAX][6];
+            T o = T(0);
+            if (DIR == HPEZ_DECOMPRESS) code = (int64_t)*cptr;
+            else o = work[idx];
+            double pt[NAX];
+            if (warp_interior) {
 #pragma unroll
                 for (int t = 0; t < NAX; t++) {
                     const int a = kind_axis<KIND>(t);
 #pragma unroll
                     for (int i = 0; i < Fam<FAM>::n; i++) v[t][i] = work[idx + Fam<FAM>::u(i) * sEv[a]];
                 }
-                double pt[NAX];
 #pragma unroll
                 for (int t = 0; t < NAX; t++) pt[t] = Fam<FAM>::combine(v[t]);
-                if (NAX == 1) pred = pt[0];
-                else if (NAX == 2) pred = DA(DM(w0, pt[0]), DM(w1, pt[NAX - 1]));
-                else pred = DA(DA(DM(w0, pt[0]), DM(w1, pt[1])), DM(w2, pt[NAX - 1]));
-                origv = (double)o;
             } else {
-                if (DIR == HPEZ_DECOMPRESS) code = (int64_t)*cptr;
-                else origv = ldv(work, idx);
-                double pt[NAX];
 #pragma unroll
                 for (int t = 0; t < NAX; t++) {
                     const int a = kind_axis<KIND>(t);
-                    pt[t] = p1d<FAM>(work, idx, crd[a], Dv[a], s, sEv[a]);
+#pragma unroll
+                    for (int i = 0; i < Fam<FAM>::n; i++) {
+                        const int u = Fam<FAM>::u(i);
+                        const int cc = crd[a] + u * s;
+                        const bool ok = u < 0 ? cc >= 0 : cc <= Dv[a] - 1;
+                        v[t][i] = work[ok ? idx + u * sEv[a] : idx];
+                    }
                 }
-                if (NAX == 1) pred = pt[0];
-                else if (NAX == 2) pred = DA(DM(w0, pt[0]), DM(w1, pt[NAX - 1]));
-                else pred = DA(DA(DM(w0, pt[0]), DM(w1, pt[1])), DM(w2, pt[NAX - 1]));
+#pragma unroll
+                for (int t = 0; t < NAX; t++) {
+                    const int a = kind_axis<KIND>(t);
+                    double xv[6];
+#pragma unroll
+                    for (int i = 0; i < 6; i++) xv[i] = i < Fam<FAM>::n ? (double)v[t][i] : 0.0;
+                    pt[t] = in_all ? Fam<FAM>::combine(v[t]) : edge_row<FAM>(xv, crd[a], Dv[a], s);
+                }
             }
+            if (NAX == 1) pred = pt[0];
+            else if (NAX == 2) pred = DA(DM(w0, pt[0]), DM(w1, pt[NAX - 1]));
+            else pred = DA(DA(DM(w0, pt[0]), DM(w1, pt[1])), DM(w2, pt[NAX - 1]));
+            origv = (double)o;
             if (DIR == HPEZ_COMPRESS) {
                 double out;
                 const int32_t c = quantize_point<ROUND>(origv, pred, bound, two_e, inv_two_e, Rd, R32, &out);
@@ -716,26 +727,20 @@ __global__ void __launch_bounds__(kCoarseThreads, 1) coarse_kernel(const __grid_
         ((uint32_t *)s_cm)[i] = ((const uint32_t *)A.commits)[i];
     __syncthreads();
     const int nwarps = (int)(gridDim.x * blockDim.x) >> 5;
-    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    const bool tprof = A.prof && blockIdx.x == 0 && threadIdx.x == 0;
-    const unsigned long long tg0 = tprof ? globaltimer() : 0;
+    // units are dealt round-robin over the CTAs: coarse stencil loads are
+    // uncoalesced (one line per lane), so the per-SM L1 request rate, not
+    // latency, bounds a group when its warps crowd onto a few SMs
+    const int gw = (int)((threadIdx.x >> 5) * gridDim.x + blockIdx.x);
     for (int g = 0; g < A.n_groups; g++) {
         const int t0 = A.coarse_groups[2 * g], t1 = A.coarse_groups[2 * g + 1];
-        for (int rep = 0; rep < (A.dbg >> 4) + 1; rep++) {
-        for (int u = gw; u < ((A.dbg & 2) ? 0 : (t1 - t0) * kItemWarps); u += nwarps) {
+        for (int u = gw; u < (t1 - t0) * kItemWarps; u += nwarps) {
             const int t = t0 + u / kItemWarps;
             const int c = A.coarse_pairs[2 * t], item = A.coarse_pairs[2 * t + 1];
             if (FAST) process_dispatch<T, C, DIR, ROUND>(A, s_cm[c], item, u % kItemWarps);
             else process_warp<T, C, DIR, ROUND, STATS>(A, s_cm[c], item, u % kItemWarps);
         }
         cluster_sync_all();
-        if (tprof && g < 32) A.prof[32 + 2 * g + rep] = globaltimer() - tg0;
-        }
     }
-    if (tprof)
-        for (int g = 0; g < A.n_groups && g < 32; g++)
-            printf("coarse group %d: pairs %d, t=%.2f %.2f us\n", g, A.coarse_groups[2 * g + 1] - A.coarse_groups[2 * g],
-                   A.prof[32 + 2 * g] * 1e-3, A.prof[33 + 2 * g] * 1e-3);
 }
 
 // TMA bulk prefetch into L2 of everything an item reads that no earlier
@@ -849,6 +854,10 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? HPEZ_FLOW_OCC * 8 / kItem
                 const int lv = s_cm.level < 12 ? s_cm.level : 11;
                 atomicMin(A.prof + 8 + 2 * lv, now - (unsigned long long)((c3 - c2) / 1.9));
                 atomicMax(A.prof + 9 + 2 * lv, now);
+                atomicAdd(A.prof + 40 + 4 * lv, (unsigned long long)(c1 - c0));
+                atomicAdd(A.prof + 41 + 4 * lv, (unsigned long long)(c2 - c1));
+                atomicAdd(A.prof + 42 + 4 * lv, (unsigned long long)(c3 - c2));
+                atomicAdd(A.prof + 43 + 4 * lv, 1ull);
             }
         }
     }
@@ -1196,7 +1205,7 @@ static int num_sms() {
     return sms;
 }
 
-constexpr uint32_t kCoarseMax = 12000;  // leading levels of at most this many points (cumulative) run on the coarse cluster
+constexpr uint32_t kCoarseMax = 80000;  // leading levels of at most this many points (cumulative) run on the coarse cluster
 constexpr int kCoarseCluster = 16;
 static int kDiagScale = 8;  // diagonal order: item window width, in units of the dependency reach
 
@@ -1858,7 +1867,7 @@ static SweepArgs base_args(Plan &p) {
     A.coarse_groups = p.d_coarse_groups;
     A.n_groups = (int32_t)(p.coarse_groups.size() / 2);
     A.prof = p.d_prof;
-    A.dbg = (getenv("HPEZ_DEBUG_NODEPS") ? 1 : 0) | (getenv("HPEZ_COARSE_REPEAT") ? 16 : 0) | (getenv("HPEZ_COARSE_SKIP") ? 2 : 0);
+    A.dbg = getenv("HPEZ_DEBUG_NODEPS") ? 1 : 0;
     A.l2_prefetch = getenv("HPEZ_L2_PREFETCH") ? atoi(getenv("HPEZ_L2_PREFETCH")) : 0;
     A.wbase = p.d_wbase;
     A.wn = p.d_wn;
@@ -1902,6 +1911,7 @@ static int plan_setup(Plan *p, cudaStream_t st) {
         if (!e) e = cudaMemset(p->d_prof, 0, 8 * sizeof(unsigned long long));
         if (!e) e = cudaMemset(p->d_prof + 8, 0xff, 24 * sizeof(unsigned long long));
         for (int l = 0; l < 12 && !e; l++) e = cudaMemset(p->d_prof + 9 + 2 * l, 0, sizeof(unsigned long long));
+        if (!e) e = cudaMemset(p->d_prof + 32, 0, 64 * sizeof(unsigned long long));
     }
     const size_t nc = std::max<size_t>(p->commits.size(), 1);
     std::vector<int32_t> clevel(nc, 0);
@@ -1986,11 +1996,12 @@ int32_t hpez_plan_num_launches(hpez_plan plan) {
 // diag_order, flow_fast, coarse_fast, dep_intervals] and, when the plan was
 // built with HPEZ_PROFILE set, the flow kernel's accumulated clock64 phase
 // counters [grab, wait, work, items] (out[8..11]).
-int hpez_plan_levels_timeline(hpez_plan plan, int64_t *out) {  // 24 values (start, end) x 12 levels
+int hpez_plan_levels_timeline(hpez_plan plan, int64_t *out) {  // 72 values, see the header
     if (!plan || !out || !plan->p.d_prof) return HPEZ_BAD_ARGUMENT;
-    unsigned long long h[24];
+    unsigned long long h[80];
     if (cudaMemcpy(h, plan->p.d_prof + 8, sizeof h, cudaMemcpyDeviceToHost) != cudaSuccess) return HPEZ_CUDA_ERROR;
     for (int i = 0; i < 24; i++) out[i] = (int64_t)h[i];
+    for (int i = 0; i < 48; i++) out[24 + i] = (int64_t)h[32 + i];
     return HPEZ_OK;
 }
 

@@ -15,12 +15,17 @@ a0[::64, ::64, ::64] = orig[::64, ::64, ::64]
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 kw = dict(radius=32768, md_alpha=md, rounding=1)
 codes = outl = None
+FL = os.environ.get("FLUSH", "write")
+def flush_op(v):
+    if FL == "write": flush.fill_(v)
+    elif FL == "read": flush.fill_(v); torch.cuda.synchronize(); flush.sum()
+    elif FL == "readonly": flush.sum()
 tc, td = [], []
 for it in range(8):
-    w.copy_(orig); flush.fill_(1.0)
+    w.copy_(orig); flush_op(1.0)
     e0, e1, e2, e3 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     e0.record(); codes, outl, n = run_levels_device(w, lv, direction="compress", sync=False, **kw); e1.record()
-    back.copy_(a0); flush.fill_(2.0)
+    back.copy_(a0); flush_op(2.0)
     e2.record(); run_levels_device(back, lv, direction="decompress", codes=codes, outliers=outl, sync=False, **kw); e3.record()
     torch.cuda.synchronize()
     if it >= 3:
