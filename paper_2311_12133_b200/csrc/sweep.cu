@@ -37,6 +37,9 @@
 #ifndef HPEZ_FLOW_OCC
 #define HPEZ_FLOW_OCC 4  // flow-kernel CTAs per SM the fast path is compiled for
 #endif
+#ifndef HPEZ_ILP2
+#define HPEZ_ILP2 1  // fast path: two interior iterations per step
+#endif
 
 namespace hpez {
 
@@ -568,21 +571,114 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
     uint32_t q = fdiv(r, cm.fd[1]);
     int jy = (int)(r - q * (uint32_t)cn1);
     int jz = (int)q;
-    for (uint32_t pb = p0; pb < pend; pb += 32) {
+    constexpr int NAX = KIND < 3 ? 1 : KIND < 6 ? 2 : 3;
+    const int Dv[3] = {D0, D1, D2};
+    const int sEv[3] = {sE0, sE1, sE2};
+    auto advance = [&](int &ax, int &ay, int &az) {
+        ax += 32;
+        while (ax >= cn2) {
+            ax -= cn2;
+            if (++ay >= cn1) {
+                ay = 0;
+                az++;
+            }
+        }
+    };
+    auto interior_at = [&](const int (&crd)[3]) {
+        bool in = true;
+#pragma unroll
+        for (int t = 0; t < NAX; t++) in &= Fam<FAM>::interior(crd[kind_axis<KIND>(t)], Dv[kind_axis<KIND>(t)], s);
+        return in;
+    };
+    auto blend = [&](const double (&pt)[NAX]) {
+        if (NAX == 1) return pt[0];
+        if (NAX == 2) return DA(DM(w0, pt[0]), DM(w1, pt[NAX - 1]));
+        return DA(DA(DM(w0, pt[0]), DM(w1, pt[1])), DM(w2, pt[NAX - 1]));
+    };
+    uint32_t pb = p0;
+#if HPEZ_ILP2
+    // two full interior iterations per step: both iterations' stencil (and
+    // original / code) loads are issued before either is consumed, halving
+    // the exposed memory latency per point
+    for (; pb + 64 <= pend; pb += 64) {
+        int bx = jx, by = jy, bz = jz;
+        advance(bx, by, bz);
+        const int cA[3] = {st0 + jz * sp0, st1 + jy * sp1, st2 + jx * sp2};
+        const int cB[3] = {st0 + bz * sp0, st1 + by * sp1, st2 + bx * sp2};
+        if (!__all_sync(0xffffffffu, interior_at(cA) && interior_at(cB))) break;
+        const int iA = cA[0] * E0 + cA[1] * E1 + cA[2], iB = cB[0] * E0 + cB[1] * E1 + cB[2];
+        T vA[NAX][6], vB[NAX][6];
+        T oA = T(0), oB = T(0);
+        int64_t kA = 0, kB = 0;
+        if (DIR == HPEZ_DECOMPRESS) {
+            kA = (int64_t)cptr[0];
+            kB = (int64_t)cptr[32];
+        } else {
+            oA = work[iA];
+            oB = work[iB];
+        }
+#pragma unroll
+        for (int t = 0; t < NAX; t++) {
+            const int a = kind_axis<KIND>(t);
+#pragma unroll
+            for (int i = 0; i < Fam<FAM>::n; i++) {
+                vA[t][i] = work[iA + Fam<FAM>::u(i) * sEv[a]];
+                vB[t][i] = work[iB + Fam<FAM>::u(i) * sEv[a]];
+            }
+        }
+        double ptA[NAX], ptB[NAX];
+#pragma unroll
+        for (int t = 0; t < NAX; t++) {
+            ptA[t] = Fam<FAM>::combine(vA[t]);
+            ptB[t] = Fam<FAM>::combine(vB[t]);
+        }
+        const double predA = blend(ptA), predB = blend(ptB);
+        bool eA = false, eB = false;
+        if (DIR == HPEZ_COMPRESS) {
+            double out;
+            int32_t c = quantize_point<ROUND>((double)oA, predA, bound, two_e, inv_two_e, Rd, R32, &out);
+            cptr[0] = (C)c;
+            eA = c == 0;
+            if (!eA) work[iA] = (T)out;
+            c = quantize_point<ROUND>((double)oB, predB, bound, two_e, inv_two_e, Rd, R32, &out);
+            cptr[32] = (C)c;
+            eB = c == 0;
+            if (!eB) work[iB] = (T)out;
+        } else {
+            eA = kA == 0;
+            eB = kB == 0;
+            if (!eA) work[iA] = (T)dequantize_point<ROUND>(predA, kA, two_e, R);
+            if (!eB) work[iB] = (T)dequantize_point<ROUND>(predB, kB, two_e, R);
+        }
+        const uint32_t ebA = __ballot_sync(0xffffffffu, eA);
+        const uint32_t ebB = __ballot_sync(0xffffffffu, eB);
+        if (DIR == HPEZ_DECOMPRESS && (ebA | ebB)) {
+            const int64_t oa = obase + nesc + __popc(ebA & ((1u << lane) - 1u));
+            const int64_t ob = obase + nesc + __popc(ebA) + __popc(ebB & ((1u << lane) - 1u));
+            if (eA) {
+                if (oa < A.outl_cap) __stcg(work + iA, (T)A.outl[oa]);
+                else atomicExch(A.flags, HPEZ_OUTLIER_UNDERFLOW);
+            }
+            if (eB) {
+                if (ob < A.outl_cap) __stcg(work + iB, (T)A.outl[ob]);
+                else atomicExch(A.flags, HPEZ_OUTLIER_UNDERFLOW);
+            }
+        }
+        nesc += __popc(ebA) + __popc(ebB);
+        cptr += 64;
+        jx = bx;
+        jy = by;
+        jz = bz;
+        advance(jx, jy, jz);
+    }
+#endif
+    for (; pb < pend; pb += 32) {
         const bool valid = pb + lane < pend;
         const int z = st0 + jz * sp0, y = st1 + jy * sp1, x = st2 + jx * sp2;
         const int idx = z * E0 + y * E1 + x;
         bool esc = false;
-        constexpr int NAX = KIND < 3 ? 1 : KIND < 6 ? 2 : 3;
         const int crd[3] = {z, y, x};
-        const int Dv[3] = {D0, D1, D2};
-        const int sEv[3] = {sE0, sE1, sE2};
-        bool in_all = true;
-#pragma unroll
-        for (int t = 0; t < NAX; t++) {
-            const int a = kind_axis<KIND>(t);
-            in_all &= Fam<FAM>::interior(crd[a], Dv[a], s);
-        }
+        const bool in_all = interior_at(crd);
         // warp-uniform split: a warp with any edge lane loads every lane's
         // stencil with in-grid (clamped) addresses, so it still costs a single
         // memory round trip; only the row arithmetic differs per lane
@@ -628,9 +724,7 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
                     pt[t] = in_all ? Fam<FAM>::combine(v[t]) : edge_row<FAM>(xv, crd[a], Dv[a], s);
                 }
             }
-            if (NAX == 1) pred = pt[0];
-            else if (NAX == 2) pred = DA(DM(w0, pt[0]), DM(w1, pt[NAX - 1]));
-            else pred = DA(DA(DM(w0, pt[0]), DM(w1, pt[1])), DM(w2, pt[NAX - 1]));
+            pred = blend(pt);
             origv = (double)o;
             if (DIR == HPEZ_COMPRESS) {
                 double out;
@@ -652,20 +746,11 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
         }
         nesc += __popc(eb);
         cptr += 32;
-        jx += 32;
-        while (jx >= cn2) {
-            jx -= cn2;
-            if (++jy >= cn1) {
-                jy = 0;
-                jz++;
-            }
-        }
+        advance(jx, jy, jz);
         if (HPEZ_L1_PREFETCH && pb + 32 + lane < pend) {
             // L1 prefetch of the next iteration's stencil lines (clamped in-grid)
-            constexpr int NAX = KIND < 3 ? 1 : KIND < 6 ? 2 : 3;
             const int nz = st0 + jz * sp0, ny = st1 + jy * sp1, nx = st2 + jx * sp2;
             const int nidx = nz * E0 + ny * E1 + nx;
-            const int sEv[3] = {sE0, sE1, sE2};
             const int last = D0 * E0 - 1;
 #pragma unroll
             for (int t = 0; t < NAX; t++) {
@@ -797,27 +882,27 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? HPEZ_FLOW_OCC * 8 / kItem
     int cur = -1;
     bool first = true;
     unsigned long long t_grab = 0, t_wait = 0, t_work = 0, n_done = 0;
-    int next_rel = 0;
-    if (threadIdx.x == 0) next_rel = atomicAdd(A.next, 1);
+    // items are claimed two steps ahead: the atomic issued while item k runs
+    // returns during its work and becomes item k + 2.  Two CTA barriers per
+    // item: B (dependencies acquired, descriptor staged) and A (item written).
+    int q_cur = 0, q_next = 0;
+    if (threadIdx.x == 0) {
+        s_item = atomicAdd(A.next, 1);
+        s_next = q_cur = atomicAdd(A.next, 1);
+        q_next = atomicAdd(A.next, 1);
+    }
+    __syncthreads();
     while (true) {
         const long long c0 = A.prof ? clock64() : 0;
-        // the next item is claimed one step ahead, so the atomic's latency
-        // overlaps the previous item's work
-        if (threadIdx.x == 0) {
-            s_item = next_rel;
-            if (next_rel < A.n_items) next_rel = atomicAdd(A.next, 1);
-            s_next = next_rel;
-        }
-        __syncthreads();
-        const int rel = s_item;
+        const int rel = s_item, nrel = s_next;
         if (rel >= A.n_items) break;
-        if (warp == 1 && A.l2_prefetch) {
-            if (first) prefetch_item<T, C, DIR>(A, A.flow_order[rel], lane);
-            if (s_next < A.n_items) prefetch_item<T, C, DIR>(A, A.flow_order[s_next], lane);
-        }
-        first = false;
         const int item = A.flow_order[rel];
         const int c = A.item_commit[item];
+        if (warp == 1 && A.l2_prefetch) {
+            if (first) prefetch_item<T, C, DIR>(A, item, lane);
+            if (nrel < A.n_items) prefetch_item<T, C, DIR>(A, A.flow_order[nrel], lane);
+        }
+        first = false;
         if (c != cur) {
             if (threadIdx.x < sizeof(CommitDev) / 4)
                 ((uint32_t *)&s_cm)[threadIdx.x] = ((const uint32_t *)&A.commits[c])[threadIdx.x];
@@ -828,20 +913,25 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? HPEZ_FLOW_OCC * 8 / kItem
             const int k0 = A.dep_off[item], k1 = A.dep_off[item + 1];
             for (int k = k0; k < k1; k++) {
                 const int2 d = A.dep_rng[k];
+                // acquire loads: no fence instruction, but each invalidates
+                // this SM's L1 (CCTL.IVALL) so the item's plain loads see the
+                // producers' writes; bar.sync below extends it to the CTA
                 for (int q = d.x + lane; q <= d.y; q += 32)
-                    while (ld_relaxed(&A.done[q]) == 0) __nanosleep(32);
+                    while (ld_acquire(&A.done[q]) == 0) __nanosleep(32);
             }
-            __threadfence();  // also invalidates this SM's L1 (CCTL.IVALL)
         }
-        __syncthreads();
+        __syncthreads();  // B
         const long long c2 = A.prof ? clock64() : 0;
         if (FAST) process_dispatch<T, C, DIR, ROUND>(A, s_cm, item, warp);
         else process_warp<T, C, DIR, ROUND, STATS>(A, s_cm, item, warp);
-        __syncthreads();  // CTA writes happen-before thread 0's gpu-scope release
-        if (threadIdx.x == 0) {
-            __threadfence();
-            st_release(&A.done[item], 1u);
+        if (threadIdx.x == 0) {  // nobody reads s_item / s_next again before barrier A
+            s_item = q_cur;
+            s_next = q_next;
+            q_cur = q_next;
+            if (q_next < A.n_items) q_next = atomicAdd(A.next, 1);
         }
+        __syncthreads();  // A: CTA writes happen-before thread 0's gpu-scope release
+        if (threadIdx.x == 0) st_release(&A.done[item], 1u);  // cumulative over the CTA's writes
         if (A.prof) {
             const long long c3 = clock64();
             t_grab += c1 - c0;
@@ -1610,6 +1700,8 @@ struct Plan {
         if (const char *ev = getenv("HPEZ_DIAG_SCALE")) kDiagScale = std::max(1, atoi(ev));
         int pmax = 512 * kItemWarps;
         if (const char *ev = getenv("HPEZ_ITEM_MAX")) pmax = std::max(256, atoi(ev));
+        int items_per_sm = 2;
+        if (const char *ev = getenv("HPEZ_ITEMS_PER_SM")) items_per_sm = std::max(1, atoi(ev));
         uint32_t coarse_max = kCoarseMax;
         if (const char *ev = getenv("HPEZ_COARSE_MAX")) coarse_max = (uint32_t)atoi(ev);
         if (const char *ev = getenv("HPEZ_COARSE_CLUSTER")) coarse_cluster = std::max(1, std::min(16, atoi(ev)));
@@ -1630,7 +1722,7 @@ struct Plan {
         int32_t item = 0;
         for (int ci = 0; ci < nc; ci++) {
             CommitDev &cm = commits[ci];
-            int64_t p = (int64_t)cm.npos / (4 * sms);
+            int64_t p = (int64_t)cm.npos / (items_per_sm * sms);
             // coarse commits: one position per lane, so a warp unit is one round trip
             p = ci < c_coarse ? 256 : std::max<int64_t>(256, std::min<int64_t>(pmax, p));
             p = (p + 255) / 256 * 256;
