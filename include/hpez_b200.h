@@ -130,6 +130,18 @@ int hpez_huffman_pack(const void *codes, int32_t code_dtype, int64_t n,
 int hpez_huffman_decode(const uint8_t *payload, int64_t nbytes, const uint8_t *lengths,
                         int64_t n_lengths, int64_t count, int32_t *out);
 
+/* huffman._unpack_symbols (huffman.py:116-141) on the device: the same
+ * `count` symbols and error statuses as hpez_huffman_decode, written to
+ * out_dev as u16 (code_dtype HPEZ_CODES_U16, n_lengths <= 65536) or int32.
+ * The payload comes from host memory (payload_host) or device memory
+ * (payload_dev); exactly one is non-NULL.  Self-synchronising chunked
+ * decode: speculative per-chunk decode, fix-up passes until every chunk
+ * starts at its predecessor's exit, scanned offsets, write pass.  Blocks
+ * the calling thread on `stream` for the pass count and the symbol total. */
+int hpez_huffman_decode_device(const uint8_t *payload_host, const uint8_t *payload_dev, int64_t nbytes,
+                               const uint8_t *lengths, int64_t n_lengths, int64_t count, void *out_dev,
+                               int32_t code_dtype, void *stream);
+
 /* tuner.tune_blocks scoring reduction (tuner.py:470-472): out[r] = numpy's
  * pairwise sum of rows[r, 0..rowlen) (= rows.sum(axis=1) bit for bit).  The
  * dense error grids come from bound-0 hpez_sweep_run trials with stats. */

@@ -72,6 +72,7 @@ def lib():
         "hpez_huffman_nbits": (I32, [P, I32, I64, P, ctypes.POINTER(I64), P]),
         "hpez_huffman_pack": (I32, [P, I32, I64, P, P, I32, P, I64, P]),
         "hpez_huffman_decode": (I32, [P, I64, P, I64, I64, P]),
+        "hpez_huffman_decode_device": (I32, [P, P, I64, P, I64, I64, P, I32, P]),
         "hpez_rows_pairwise_sum": (I32, [P, I64, I64, P, P]),
         "hpez_set_device": (I32, [I32]),
         "hpez_build_info": (ctypes.c_char_p, []),

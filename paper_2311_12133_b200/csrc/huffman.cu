@@ -9,8 +9,9 @@
 // * pack: chunks of 4096 codes; per-chunk bit counts -> scan -> each CTA
 //   assembles its chunk MSB-first in shared memory with atomicOr and stores
 //   whole 32-bit words, OR-ing only the two boundary words globally.
-// * decode: host table-driven canonical decoder (12-bit first-level LUT,
-//   bit-serial continuation) with the reference's error semantics.
+// * decode: self-synchronising chunked device decoder (speculative chunk
+//   decode, fix-up passes, scanned offsets, write pass) and a host
+//   table-driven decoder, both with the reference's error semantics.
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -18,6 +19,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace hpez {
 
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(1024) scan_u64_kernel(uint64_t *v, int64_t n, 
     }
     if (threadIdx.x == 0 && total) *total = s_carry;
 }
+
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
@@ -272,6 +275,301 @@ static int build_table(const int64_t *freqs, int64_t n, uint8_t *lengths, uint64
 
 using namespace hpez;
 
+// Canonical decode tables (huffman.canonical_codes, huffman.py:51-88) with
+// the reference's validity rules, shared by the host and device decoders.
+constexpr int kLutBits = 12;
+struct Canon {
+    int maxl = 0;
+    int64_t present = 0;
+    std::vector<int64_t> cnt, first_code, first_rank;
+    std::vector<int32_t> rank_sym;
+    std::vector<int32_t> lut_sym;  // 12-bit prefix -> symbol (codes <= 12 bits)
+    std::vector<uint8_t> lut_len;  // 0 = prefix of a longer code
+};
+
+static int build_canon(const uint8_t *lengths, int64_t n_lengths, Canon &t) {
+    t.cnt.assign(258, 0);
+    for (int64_t s = 0; s < n_lengths; s++)
+        if (lengths[s]) {
+            t.cnt[lengths[s]]++;
+            t.present++;
+            t.maxl = std::max(t.maxl, (int)lengths[s]);
+        }
+    if (t.present == 0 || t.maxl > 64) return HPEZ_INVALID_TABLE;
+    if (t.present == 1) {
+        if (t.maxl != 1) return HPEZ_INVALID_TABLE;
+    } else {
+        // Kraft equality sum cnt[l] * 2^(maxl-l) == 2^maxl (exact in 128-bit)
+        unsigned __int128 k = 0;
+        for (int l = 1; l <= t.maxl; l++) k += (unsigned __int128)t.cnt[l] << (t.maxl - l);
+        if (k != ((unsigned __int128)1 << t.maxl)) return HPEZ_INVALID_TABLE;
+    }
+    t.first_code.assign(t.maxl + 2, 0);
+    t.first_rank.assign(t.maxl + 2, 0);
+    int64_t code = 0, rank = 0;
+    for (int l = 1; l <= t.maxl; l++) {
+        t.first_code[l] = code;
+        t.first_rank[l] = rank;
+        code = (code + t.cnt[l]) << 1;
+        rank += t.cnt[l];
+    }
+    t.rank_sym.resize((size_t)rank);
+    std::vector<int64_t> fill(t.first_rank.begin(), t.first_rank.end());
+    for (int64_t s = 0; s < n_lengths; s++)
+        if (lengths[s]) t.rank_sym[(size_t)fill[lengths[s]]++] = (int32_t)s;
+    t.lut_sym.assign(1 << kLutBits, -1);
+    t.lut_len.assign(1 << kLutBits, 0);
+    for (int l = 1; l <= std::min(t.maxl, kLutBits); l++)
+        for (int64_t r = 0; r < t.cnt[l]; r++) {
+            const int64_t c = t.first_code[l] + r;
+            const int64_t lo = c << (kLutBits - l), hi = (c + 1) << (kLutBits - l);
+            for (int64_t q = lo; q < hi; q++) {
+                t.lut_sym[(size_t)q] = t.rank_sym[(size_t)(t.first_rank[l] + r)];
+                t.lut_len[(size_t)q] = (uint8_t)l;
+            }
+        }
+    return HPEZ_OK;
+}
+
+// ------------------------------------------------------ device decoder --
+// Self-synchronising chunked decode of the single MSB-first stream (no
+// format change).  The payload is cut into chunks of kDecChunk bits; chunk
+// k owns the codewords that START in its bit range, so its true start is the
+// first codeword boundary at or after its first bit, which is where its
+// predecessor's decode exits.
+//   1. spec: every chunk is decoded from its first bit (assumed boundary);
+//      the first kDecMarks symbol starts of that path are recorded.
+//   2. fix: each chunk restarts at its predecessor's exit and decodes only
+//      until it lands on one of its recorded speculative starts (Huffman codes
+//      resynchronise within a few codewords), then takes the speculative
+//      count and exit from there.  Repeated until no chunk changes (one pass
+//      in practice; pass i fixes chunk i at the latest).
+//   3. exclusive scan of the per-chunk counts -> output offsets; total.
+//   4. write: every chunk decodes from its true start into a shared-memory
+//      stage laid out in output order, copied out coalesced.
+// Complete (Kraft-equal) tables decode every bit string, so speculation
+// never hits an invalid pattern.  Bits are read through a 4-word register
+// window refilled one 32-bit word at a time.
+constexpr int kDecChunk = 1024;   // bits per chunk (> 64, the longest code)
+constexpr int kDecThreads = 256;  // spec / fix CTAs
+constexpr int kDecWriteThreads = 128;
+constexpr int kDecLut = 11;       // first-level table bits on the device
+constexpr int kDecMarks = 16;     // speculative symbol starts kept per chunk
+constexpr int kDecStage = 24576;  // staged output symbols per write CTA
+
+struct DecDev {
+    uint64_t limit[66];  // first_code[l] + cnt[l]: l-bit prefixes below it are codes
+    uint64_t first_code[66];
+    int64_t first_rank[66];
+    int32_t maxl, pad;
+    int32_t lut_sym[1 << kDecLut];
+    uint8_t lut_len[1 << kDecLut];
+};
+
+
+struct BitReader {
+    const uint32_t *__restrict__ w;
+    int64_t wi;  // word index of a
+    uint32_t a, b, c, d;
+    __device__ __forceinline__ void init(const uint32_t *__restrict__ words, int64_t pos) {
+        w = words;
+        wi = pos >> 5;
+        a = bswap32(w[wi]);
+        b = bswap32(w[wi + 1]);
+        c = bswap32(w[wi + 2]);
+        d = bswap32(w[wi + 3]);
+    }
+    // 64 stream bits from `pos` (pos >> 5 == wi), MSB first
+    __device__ __forceinline__ uint64_t peek(int64_t pos) const {
+        const int sh = (int)(pos & 31);
+        const uint64_t hi = ((uint64_t)a << 32) | b;
+        return sh ? (hi << sh) | (uint64_t)(c >> (32 - sh)) : hi;
+    }
+    __device__ __forceinline__ void advance_to(int64_t pos) {
+        while ((pos >> 5) > wi) {
+            a = b;
+            b = c;
+            c = d;
+            d = bswap32(w[wi + 4]);
+            wi++;
+        }
+    }
+};
+
+// one codeword at the head of `win`: its length (0 = no code) and symbol
+__device__ __forceinline__ int dec_symbol(const DecDev &T, const int32_t *__restrict__ rank_sym, uint64_t win,
+                                          int32_t &sym) {
+    const uint32_t p = (uint32_t)(win >> (64 - kDecLut));
+    int len = T.lut_len[p];
+    sym = T.lut_sym[p];
+    if (len) return len;
+    for (int l = kDecLut + 1; l <= T.maxl; l++) {
+        const uint64_t cw = win >> (64 - l);
+        if (cw < T.limit[l]) {
+            sym = rank_sym[T.first_rank[l] + (int64_t)(cw - T.first_code[l])];
+            return l;
+        }
+    }
+    return 0;
+}
+
+__device__ __forceinline__ void load_tables(DecDev &S, const DecDev *__restrict__ G) {
+    const uint32_t *src = (const uint32_t *)G;
+    uint32_t *dst = (uint32_t *)&S;
+    for (int i = threadIdx.x; i < (int)(sizeof(DecDev) / 4); i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+}
+
+// pass 1: speculative decode of every chunk from its first bit
+__global__ void __launch_bounds__(kDecThreads) dec_spec_kernel(const uint32_t *__restrict__ w, int64_t nbits,
+                                                               int64_t nchunks, const DecDev *__restrict__ tab,
+                                                               const int32_t *__restrict__ rank_sym,
+                                                               uint16_t *__restrict__ marks,
+                                                               int32_t *__restrict__ spec_cnt,
+                                                               int64_t *__restrict__ spec_exit,
+                                                               int64_t *__restrict__ start, int32_t *__restrict__ cnt,
+                                                               int64_t *__restrict__ exit, uint32_t *flags) {
+    __shared__ DecDev S;
+    load_tables(S, tab);
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nchunks) return;
+    const int64_t a = k * kDecChunk, end = min(a + kDecChunk, nbits);
+    BitReader br;
+    br.init(w, a);
+    int64_t pos = a;
+    int32_t n = 0;
+    while (pos < end) {
+        if (n < kDecMarks) marks[k * kDecMarks + n] = (uint16_t)(pos - a);
+        int32_t sym;
+        const int len = dec_symbol(S, rank_sym, br.peek(pos), sym);
+        if (!len) {  // unreachable for complete tables
+            atomicOr(flags, 1u);
+            break;
+        }
+        if (pos + len > nbits) break;  // codeword cut off by the end of the payload
+        n++;
+        pos += len;
+        br.advance_to(pos);
+    }
+    spec_cnt[k] = cnt[k] = n;
+    spec_exit[k] = exit[k] = pos;
+    start[k] = a;
+}
+
+// pass 2 (repeated while anything changes): restart at the predecessor's exit
+__global__ void __launch_bounds__(kDecThreads) dec_fix_kernel(const uint32_t *__restrict__ w, int64_t nbits,
+                                                              int64_t nchunks, const DecDev *__restrict__ tab,
+                                                              const int32_t *__restrict__ rank_sym,
+                                                              const uint16_t *__restrict__ marks,
+                                                              const int32_t *__restrict__ spec_cnt,
+                                                              const int64_t *__restrict__ spec_exit,
+                                                              int64_t *__restrict__ start, int32_t *__restrict__ cnt,
+                                                              const int64_t *__restrict__ exit_in,
+                                                              int64_t *__restrict__ exit_out, uint32_t *flags,
+                                                              uint32_t *changed) {
+    __shared__ DecDev S;
+    load_tables(S, tab);
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nchunks) return;
+    const int64_t a = k ? exit_in[k - 1] : 0;
+    if (a == start[k]) {
+        exit_out[k] = exit_in[k];
+        return;
+    }
+    *changed = 1u;
+    start[k] = a;
+    const int64_t base = k * kDecChunk, end = min(base + kDecChunk, nbits);
+    if (a >= end) {
+        cnt[k] = 0;
+        exit_out[k] = a;
+        return;
+    }
+    const int nsp = spec_cnt[k];
+    const int nm = min(nsp, kDecMarks);
+    BitReader br;
+    br.init(w, a);
+    int64_t pos = a;
+    int32_t n = 0;
+    int i = 0;
+    while (pos < end) {
+        while (i < nm && base + marks[k * kDecMarks + i] < pos) i++;
+        if (i < nm && base + marks[k * kDecMarks + i] == pos) {  // joined the speculative path
+            cnt[k] = n + (nsp - i);
+            exit_out[k] = spec_exit[k];
+            return;
+        }
+        int32_t sym;
+        const int len = dec_symbol(S, rank_sym, br.peek(pos), sym);
+        if (!len) {
+            atomicOr(flags, 1u);
+            break;
+        }
+        if (pos + len > nbits) break;
+        n++;
+        pos += len;
+        br.advance_to(pos);
+    }
+    cnt[k] = n;
+    exit_out[k] = pos;
+}
+
+// pass 4: decode from the true starts into an output-ordered stage
+template <typename O>
+__global__ void __launch_bounds__(kDecWriteThreads) dec_write_kernel(const uint32_t *__restrict__ w, int64_t nbits,
+                                                                     int64_t nchunks, const DecDev *__restrict__ tab,
+                                                                     const int32_t *__restrict__ rank_sym,
+                                                                     const int64_t *__restrict__ start,
+                                                                     const int32_t *__restrict__ cnt,
+                                                                     const int64_t *__restrict__ off, int64_t count,
+                                                                     O *__restrict__ out) {
+    __shared__ DecDev S;
+    extern __shared__ __align__(16) unsigned char s_stage_raw[];
+    O *stage = reinterpret_cast<O *>(s_stage_raw);
+    const int64_t k0 = (int64_t)blockIdx.x * kDecWriteThreads;
+    const int64_t kl = min(k0 + kDecWriteThreads, nchunks) - 1;
+    const int64_t b0 = off[k0];
+    if (b0 >= count) return;  // uniform over the CTA
+    load_tables(S, tab);
+    const int64_t b1 = min(off[kl] + cnt[kl], count);
+    const bool staged = b1 - b0 <= kDecStage;
+    const int64_t k = k0 + threadIdx.x;
+    if (k <= kl && off[k] < count) {
+        const int64_t a = start[k], end = min((k + 1) * (int64_t)kDecChunk, nbits);
+        int64_t o = off[k];
+        const int64_t o1 = min(o + cnt[k], count);
+        BitReader br;
+        br.init(w, a);
+        int64_t pos = a;
+        while (o < o1) {
+            int32_t sym;
+            const int len = dec_symbol(S, rank_sym, br.peek(pos), sym);
+            if (staged) stage[o - b0] = (O)sym;
+            else out[o] = (O)sym;
+            o++;
+            pos += len;
+            br.advance_to(pos);
+        }
+        (void)end;
+    }
+    if (!staged) return;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < b1 - b0; i += kDecWriteThreads) out[b0 + i] = stage[i];
+}
+
+// single-symbol tables (the only incomplete tree the reference accepts):
+// every symbol is the bit 0; find the first 1 bit
+__global__ void dec_first_one_kernel(const uint8_t *__restrict__ p, int64_t nbytes, unsigned long long *first) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nbytes || !p[i]) return;
+    atomicMin(first, (unsigned long long)(i * 8 + (__clz((int)p[i]) - 24)));
+}
+
+template <typename O>
+__global__ void dec_fill_kernel(O *__restrict__ out, int64_t n, O v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = v;
+}
+
 extern "C" {
 
 int hpez_histogram(const void *codes, int32_t code_dtype, int64_t n, uint32_t *counts, int64_t nbins,
@@ -363,64 +661,24 @@ int hpez_huffman_decode(const uint8_t *payload, int64_t nbytes, const uint8_t *l
                         int64_t count, int32_t *out) {
     if (count == 0) return HPEZ_OK;
     if (!lengths || !out || n_lengths <= 0) return HPEZ_BAD_ARGUMENT;
-    // canonical tables + validity (huffman.canonical_codes, huffman.py:51-88)
-    int maxl = 0;
-    int64_t present = 0;
-    std::vector<int64_t> cnt(258, 0);
-    for (int64_t s = 0; s < n_lengths; s++)
-        if (lengths[s]) {
-            cnt[lengths[s]]++;
-            present++;
-            maxl = std::max(maxl, (int)lengths[s]);
-        }
-    if (present == 0 || maxl > 64) return HPEZ_INVALID_TABLE;
-    if (present == 1) {
-        if (maxl != 1) return HPEZ_INVALID_TABLE;
-    } else {
-        // Kraft equality sum cnt[l] * 2^(maxl-l) == 2^maxl (exact in 128-bit)
-        unsigned __int128 k = 0;
-        for (int l = 1; l <= maxl; l++) k += (unsigned __int128)cnt[l] << (maxl - l);
-        if (k != ((unsigned __int128)1 << maxl)) return HPEZ_INVALID_TABLE;
-    }
-    std::vector<int64_t> first_code(maxl + 2, 0), first_rank(maxl + 2, 0);
-    int64_t code = 0, rank = 0;
-    for (int l = 1; l <= maxl; l++) {
-        first_code[l] = code;
-        first_rank[l] = rank;
-        code = (code + cnt[l]) << 1;
-        rank += cnt[l];
-    }
-    std::vector<int32_t> rank_sym((size_t)rank);
-    {
-        std::vector<int64_t> fill(first_rank.begin(), first_rank.end());
-        for (int64_t s = 0; s < n_lengths; s++)
-            if (lengths[s]) rank_sym[(size_t)fill[lengths[s]]++] = (int32_t)s;
-    }
-    constexpr int K = 12;
-    struct Lut { int32_t sym; int8_t len; };
-    std::vector<Lut> lut(1 << K, Lut{-1, 0});
-    for (int l = 1; l <= std::min(maxl, K); l++)
-        for (int64_t r = 0; r < cnt[l]; r++) {
-            const int64_t c = first_code[l] + r;
-            const int64_t lo = c << (K - l), hi = (c + 1) << (K - l);
-            for (int64_t p = lo; p < hi; p++) lut[(size_t)p] = Lut{rank_sym[(size_t)(first_rank[l] + r)], (int8_t)l};
-        }
+    Canon t;
+    if (int st = build_canon(lengths, n_lengths, t)) return st;
+    const int maxl = t.maxl;
     const int64_t nbits = nbytes * 8;
     int64_t bitpos = 0;
     auto peek = [&](int64_t pos, int k) -> uint32_t {  // k bits at pos, zero padded
-        uint32_t v = 0;
         const int64_t byte = pos >> 3;
         uint64_t w = 0;
         for (int b = 0; b < 4; b++) w = (w << 8) | (byte + b < nbytes ? payload[byte + b] : 0);
         w <<= (pos & 7);
-        v = (uint32_t)((w >> (32 - k)) & ((1u << k) - 1));
-        return v;
+        return (uint32_t)((w >> (32 - k)) & ((1u << k) - 1));
     };
     for (int64_t i = 0; i < count; i++) {
-        const Lut e = lut[peek(bitpos, K)];
-        if (e.len > 0 && bitpos + e.len <= nbits) {
-            out[i] = e.sym;
-            bitpos += e.len;
+        const uint32_t q = peek(bitpos, kLutBits);
+        const int len0 = t.lut_len[q];
+        if (len0 > 0 && bitpos + len0 <= nbits) {
+            out[i] = t.lut_sym[q];
+            bitpos += len0;
             continue;
         }
         // bit-serial continuation, identical control flow to the reference
@@ -433,16 +691,162 @@ int hpez_huffman_decode(const uint8_t *payload, int64_t nbytes, const uint8_t *l
             c = (c << 1) | bit;
             len++;
             if (len > maxl) return HPEZ_INVALID_TABLE;
-            if (cnt[len] > 0) {
-                const int64_t off = c - first_code[len];
-                if (off >= 0 && off < cnt[len]) {
-                    out[i] = rank_sym[(size_t)(first_rank[len] + off)];
+            if (t.cnt[len] > 0) {
+                const int64_t off = c - t.first_code[len];
+                if (off >= 0 && off < t.cnt[len]) {
+                    out[i] = t.rank_sym[(size_t)(t.first_rank[len] + off)];
                     break;
                 }
             }
         }
     }
     return HPEZ_OK;
+}
+
+// Device decode of `count` symbols into out_dev (u16 or i32).  The payload
+// is copied to the device from host memory (payload_host) or read from
+// device memory (payload_dev, nbytes + 12 readable bytes, zero padded).
+int hpez_huffman_decode_device(const uint8_t *payload_host, const uint8_t *payload_dev, int64_t nbytes,
+                               const uint8_t *lengths, int64_t n_lengths, int64_t count, void *out_dev,
+                               int32_t out_dtype, void *stream) {
+    if (count == 0) return HPEZ_OK;
+    if (!lengths || !out_dev || n_lengths <= 0 || (!payload_host && !payload_dev && nbytes > 0)) return HPEZ_BAD_ARGUMENT;
+    if (out_dtype != HPEZ_CODES_U16 && out_dtype != HPEZ_CODES_I32) return HPEZ_BAD_ARGUMENT;
+    if (out_dtype == HPEZ_CODES_U16 && n_lengths > 65536) return HPEZ_BAD_ARGUMENT;
+    Canon t;
+    if (int st = build_canon(lengths, n_lengths, t)) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nbits = nbytes * 8;
+    const int64_t nwords = (nbytes + 3) / 4 + 6;  // BitReader reads up to 5 words ahead
+    uint32_t *w = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&w, (size_t)nwords * 4, s);
+    if (e) return cuda_ok(e);
+    e = cudaMemsetAsync(w, 0, (size_t)nwords * 4, s);
+    if (!e && nbytes)
+        e = payload_dev ? cudaMemcpyAsync(w, payload_dev, (size_t)nbytes, cudaMemcpyDeviceToDevice, s)
+                        : cudaMemcpyAsync(w, payload_host, (size_t)nbytes, cudaMemcpyHostToDevice, s);
+    int status = HPEZ_OK;
+    if (t.present == 1) {
+        // one symbol, code "0": the reference fails at the first 1 bit
+        // (InvalidTable, or TruncatedStream if it is the last payload bit)
+        // or when the payload holds fewer than count bits
+        unsigned long long *d_first = nullptr, h_first = ~0ull;
+        if (!e) e = cudaMallocAsync((void **)&d_first, sizeof h_first, s);
+        if (!e) e = cudaMemcpyAsync(d_first, &h_first, sizeof h_first, cudaMemcpyHostToDevice, s);
+        if (!e && nbytes)
+            dec_first_one_kernel<<<(unsigned)((nbytes + 255) / 256), 256, 0, s>>>((const uint8_t *)w, nbytes, d_first);
+        if (!e) e = cudaMemcpyAsync(&h_first, d_first, sizeof h_first, cudaMemcpyDeviceToHost, s);
+        if (!e) e = cudaStreamSynchronize(s);
+        const int32_t sym = t.rank_sym[0];
+        if (!e) {
+            const int64_t j = (int64_t)h_first;
+            if (h_first != ~0ull && j < std::min(count, nbits)) status = j + 1 >= nbits ? HPEZ_TRUNCATED : HPEZ_INVALID_TABLE;
+            else if (nbits < count) status = HPEZ_TRUNCATED;
+        }
+        if (!e && status == HPEZ_OK) {
+            const unsigned g = (unsigned)((count + 255) / 256);
+            if (out_dtype == HPEZ_CODES_U16) dec_fill_kernel<<<g, 256, 0, s>>>((uint16_t *)out_dev, count, (uint16_t)sym);
+            else dec_fill_kernel<<<g, 256, 0, s>>>((int32_t *)out_dev, count, sym);
+            e = cudaGetLastError();
+        }
+        if (d_first) cudaFreeAsync(d_first, s);
+        cudaFreeAsync(w, s);
+        return e ? cuda_ok(e) : status;
+    }
+    // device tables: canonical limits + an 11-bit first-level table
+    DecDev *h_tab = new DecDev();
+    std::memset(h_tab, 0, sizeof(DecDev));
+    h_tab->maxl = t.maxl;
+    for (int l = 1; l <= t.maxl; l++) {
+        h_tab->first_code[l] = (uint64_t)t.first_code[l];
+        h_tab->limit[l] = (uint64_t)(t.first_code[l] + t.cnt[l]);
+        h_tab->first_rank[l] = t.first_rank[l];
+    }
+    for (int l = 1; l <= std::min(t.maxl, kDecLut); l++)
+        for (int64_t r = 0; r < t.cnt[l]; r++) {
+            const int64_t c = t.first_code[l] + r;
+            for (int64_t q = c << (kDecLut - l); q < (c + 1) << (kDecLut - l); q++) {
+                h_tab->lut_sym[q] = t.rank_sym[(size_t)(t.first_rank[l] + r)];
+                h_tab->lut_len[q] = (uint8_t)l;
+            }
+        }
+    const int64_t nchunks = std::max<int64_t>(1, (nbits + kDecChunk - 1) / kDecChunk);
+    DecDev *d_tab = nullptr;
+    int32_t *d_rank = nullptr, *d_cnt = nullptr, *d_spec_cnt = nullptr;
+    uint16_t *d_marks = nullptr;
+    int64_t *d_start = nullptr, *d_exit = nullptr, *d_exit2 = nullptr, *d_spec_exit = nullptr, *d_off = nullptr,
+            *d_tmp = nullptr;
+    // d_res: [0] total symbols, [1] invalid-pattern flag, [2..] changed flag per fix pass
+    constexpr int kFixPasses = 2;
+    int64_t *d_res = nullptr;
+    int64_t h_res[2 + kFixPasses] = {};
+    if (!e) e = cudaMallocAsync((void **)&d_tab, sizeof(DecDev), s);
+    if (!e) e = cudaMallocAsync((void **)&d_rank, t.rank_sym.size() * 4, s);
+    if (!e) e = cudaMallocAsync((void **)&d_marks, (size_t)nchunks * kDecMarks * 2, s);
+    if (!e) e = cudaMallocAsync((void **)&d_spec_cnt, (size_t)nchunks * 4, s);
+    if (!e) e = cudaMallocAsync((void **)&d_cnt, (size_t)nchunks * 4, s);
+    if (!e) e = cudaMallocAsync((void **)&d_spec_exit, (size_t)nchunks * 8, s);
+    if (!e) e = cudaMallocAsync((void **)&d_start, (size_t)nchunks * 8, s);
+    if (!e) e = cudaMallocAsync((void **)&d_exit, (size_t)nchunks * 8, s);
+    if (!e) e = cudaMallocAsync((void **)&d_exit2, (size_t)nchunks * 8, s);
+    if (!e) e = cudaMallocAsync((void **)&d_off, (size_t)nchunks * 8, s);
+    if (!e) e = cudaMallocAsync((void **)&d_tmp, (size_t)scan_tmp_size(nchunks) * 8, s);
+    if (!e) e = cudaMallocAsync((void **)&d_res, sizeof h_res, s);
+    if (!e) e = cudaMemcpyAsync(d_tab, h_tab, sizeof(DecDev), cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemcpyAsync(d_rank, t.rank_sym.data(), t.rank_sym.size() * 4, cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemsetAsync(d_res, 0, sizeof h_res, s);
+    uint32_t *d_invalid = (uint32_t *)(d_res + 1);
+    const unsigned grid = (unsigned)((nchunks + kDecThreads - 1) / kDecThreads);
+    auto fix = [&](uint32_t *changed) {
+        dec_fix_kernel<<<grid, kDecThreads, 0, s>>>(w, nbits, nchunks, d_tab, d_rank, d_marks, d_spec_cnt,
+                                                    d_spec_exit, d_start, d_cnt, d_exit, d_exit2, d_invalid,
+                                                    changed);
+        std::swap(d_exit, d_exit2);
+    };
+    if (!e) {
+        dec_spec_kernel<<<grid, kDecThreads, 0, s>>>(w, nbits, nchunks, d_tab, d_rank, d_marks, d_spec_cnt,
+                                                     d_spec_exit, d_start, d_cnt, d_exit, d_invalid);
+        for (int i = 0; i < kFixPasses; i++) fix((uint32_t *)(d_res + 2 + i));
+        exclusive_scan(d_cnt, nchunks, d_off, d_tmp, d_res, s);
+        e = cudaGetLastError();
+    }
+    // one host round trip in the common case: the last fix pass changed nothing
+    if (!e) e = cudaMemcpyAsync(h_res, d_res, sizeof h_res, cudaMemcpyDeviceToHost, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    for (int64_t it = kFixPasses; !e && h_res[1 + kFixPasses]; it++) {
+        if (it > nchunks + 1) {  // cannot happen: pass i fixes chunk i at the latest
+            e = cudaErrorUnknown;
+            break;
+        }
+        e = cudaMemsetAsync(d_res + 1 + kFixPasses, 0, 8, s);
+        fix((uint32_t *)(d_res + 1 + kFixPasses));
+        exclusive_scan(d_cnt, nchunks, d_off, d_tmp, d_res, s);
+        if (!e) e = cudaMemcpyAsync(h_res, d_res, sizeof h_res, cudaMemcpyDeviceToHost, s);
+        if (!e) e = cudaStreamSynchronize(s);
+    }
+    if (!e && (uint32_t)h_res[1]) status = HPEZ_INVALID_TABLE;
+    if (!e && status == HPEZ_OK && h_res[0] < count) status = HPEZ_TRUNCATED;
+    if (!e && status == HPEZ_OK) {
+        const unsigned wgrid = (unsigned)((nchunks + kDecWriteThreads - 1) / kDecWriteThreads);
+        if (out_dtype == HPEZ_CODES_U16) {
+            const size_t smem = kDecStage * sizeof(uint16_t);
+            cudaFuncSetAttribute(dec_write_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            dec_write_kernel<uint16_t><<<wgrid, kDecWriteThreads, smem, s>>>(w, nbits, nchunks, d_tab, d_rank, d_start,
+                                                                            d_cnt, d_off, count, (uint16_t *)out_dev);
+        } else {
+            const size_t smem = kDecStage * sizeof(int32_t);
+            cudaFuncSetAttribute(dec_write_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            dec_write_kernel<int32_t><<<wgrid, kDecWriteThreads, smem, s>>>(w, nbits, nchunks, d_tab, d_rank, d_start,
+                                                                           d_cnt, d_off, count, (int32_t *)out_dev);
+        }
+        e = cudaGetLastError();
+    }
+    for (void *q : {(void *)w, (void *)d_tab, (void *)d_rank, (void *)d_marks, (void *)d_spec_cnt, (void *)d_cnt,
+                    (void *)d_spec_exit, (void *)d_start, (void *)d_exit, (void *)d_exit2, (void *)d_off,
+                    (void *)d_tmp, (void *)d_res})
+        if (q) cudaFreeAsync(q, s);
+    delete h_tab;  // pageable H2D copies have consumed it by the synchronize above
+    return e ? cuda_ok(e) : status;
 }
 
 }  // extern "C"

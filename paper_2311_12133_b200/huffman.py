@@ -3,8 +3,9 @@ huffman.encode / decode (huffman.py:144-174).
 
 encode: GPU histogram (warp-aggregated, csrc/huffman.cu) -> host heap
 lengths + canonical codes (C++, same (freq, smallest-symbol) tie-break) ->
-GPU MSB-first pack.  decode: host C++ table-driven decoder.  Output bytes,
-lengths and bit counts equal the reference's.
+GPU MSB-first pack.  decode: self-synchronising chunked GPU decoder
+(decode_device) or the host C++ table-driven decoder (decode).  Output bytes,
+lengths, bit counts, symbols and error classes equal the reference's.
 """
 
 from __future__ import annotations
@@ -105,4 +106,30 @@ def decode_int32(lengths, payload: bytes, count: int) -> np.ndarray:
     buf = data.ctypes.data if data.size else None
     check(lib().hpez_huffman_decode(buf, data.size, lengths.ctypes.data, lengths.size, count,
                                     out.ctypes.data), "hpez_huffman_decode")
+    return out
+
+
+def decode_device(lengths, payload, count: int, code_dtype: int | None = None):
+    """huffman.decode on the device: ``count`` symbols as a CUDA tensor (u16
+    when every table symbol fits, else int32).  ``payload`` is bytes or a
+    device uint8 tensor."""
+    lengths = np.ascontiguousarray(np.asarray(lengths).astype(np.uint8))
+    if code_dtype is None:
+        code_dtype = _lib.CODES_U16 if lengths.size <= 65536 else _lib.CODES_I32
+    tdt = torch.uint16 if code_dtype == _lib.CODES_U16 else torch.int32
+    out = torch.empty(max(count, 1), dtype=tdt, device=device())[:count]
+    if count == 0:
+        return out
+    bind()
+    if isinstance(payload, torch.Tensor):
+        nbytes = payload.numel()
+        host, dev = None, (ptr(payload) if nbytes else None)
+    else:
+        data = np.frombuffer(payload, dtype=np.uint8)
+        nbytes = data.size
+        host, dev = (data.ctypes.data if nbytes else None), None
+        if host is None and dev is None:
+            dev = ptr(out)  # never read: nbytes == 0
+    check(lib().hpez_huffman_decode_device(host, dev, nbytes, lengths.ctypes.data, lengths.size, count,
+                                           ptr(out), code_dtype, stream()), "hpez_huffman_decode_device")
     return out

@@ -31,6 +31,11 @@ t0 = time.perf_counter(); lengths, payload, nbits = huffman.encode_device(codes)
 out["payload_MB"] = len(payload) / 1e6; out["bits_per_code"] = nbits / codes.numel()
 t0 = time.perf_counter(); dec = huffman.decode_int32(lengths, payload, codes.numel()); out["huffman_decode_host_ms"] = 1e3 * (time.perf_counter() - t0)
 assert np.array_equal(dec, codes.view(torch.int16).cpu().numpy().view(np.uint16).astype(np.int32))
+pay_dev = torch.from_numpy(np.frombuffer(payload, np.uint8).copy()).to(dev)
+t, dd = ev_time(lambda: huffman.decode_device(lengths, pay_dev, codes.numel()))
+out["huffman_decode_device_ms"] = t
+assert torch.equal(dd, codes)
+t0 = time.perf_counter(); dd = huffman.decode_device(lengths, payload, codes.numel()); torch.cuda.synchronize(); out["huffman_decode_device_from_host_wall_ms"] = 1e3 * (time.perf_counter() - t0)
 # Lorenzo
 for order in (1, 2):
     w2 = orig.clone()
