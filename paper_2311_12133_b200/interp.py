@@ -168,7 +168,10 @@ def get_plan(dims, levels, *, direction, radius, frozen_axes=(), md_alpha=None,
     key.update(bytes(lv))
     key.update(b"" if md is None else md.tobytes())
     key.update(b"" if tbl is None else tbl.tobytes())
-    key.update(str(torch.cuda.current_device()).encode())
+    # a plan owns its run scratch (escape counts, flags, counters), so each
+    # (device, stream) pair gets its own instance: sweeps on different
+    # streams may run concurrently
+    key.update(f"{torch.cuda.current_device()}:{torch.cuda.current_stream().cuda_stream}".encode())
     k = key.digest()
     plan = _PLANS.get(k)
     if plan is not None:
