@@ -97,6 +97,17 @@ int hpez_sweep_run(hpez_plan plan, void *work, void *codes, int64_t codes_avail,
  * exceed outl_cap -> rerun with a larger buffer; decompress: consumed) and
  * the sweep status (OUTLIER_UNDERFLOW on an exhausted outlier stream). */
 int hpez_sweep_finish(hpez_plan plan, void *stream, int64_t *n_outliers);
+/* Compress out of place: the pipeline's `work = f64(grid)` copy
+ * (pipeline.py:82) folded into the sweep.  Originals are read from `orig`
+ * (never written); `work` receives the anchors and every reconstructed
+ * point (escapes: their originals).  The plan must cover every non-anchor
+ * point (the reference's level ladder) -> else BAD_ARGUMENT.  Decompress
+ * plans ignore `orig`.  Otherwise as hpez_sweep_run. */
+int hpez_sweep_run_from(hpez_plan plan, const void *orig, void *work, void *codes, int64_t codes_avail,
+                        double *outliers, int64_t outl_cap, void *stream);
+/* Tiled levels of the plan (tile.cu): out[0] = count, then per level
+ * [first commit, grid, threads, smem bytes, TY, TX, ZC, intervals]. */
+int hpez_plan_tile_info(hpez_plan plan, int64_t *out, int32_t cap);
 
 /* Replaces lorenzo.lorenzo_pass (lorenzo.py:145-179) on a device grid.
  * Compress writes codes[N] and outliers; decompress reads them. */

@@ -31,6 +31,8 @@
 
 #include "common.cuh"
 #include "scan.cuh"
+#include "stencil.cuh"
+#include "tile.h"
 
 #ifndef HPEZ_L1_PREFETCH
 #define HPEZ_L1_PREFETCH 0  // measured slower on B200 (kept for experiments)
@@ -147,8 +149,7 @@ __device__ __forceinline__ double ldv(const T *__restrict__ w, int64_t i) {
     return (double)w[i];
 }
 
-#define DM(a, b) __dmul_rn((a), (b))
-#define DA(a, b) __dadd_rn((a), (b))
+// DM / DA: separately rounded f64 multiply / add (stencil.cuh)
 
 // Generic row through the constant table (edges; any family).
 template <typename T>
@@ -285,6 +286,7 @@ struct SweepArgs {
     const uint8_t *slots;
     const uint8_t *table;
     void *work;
+    const void *orig;           // compress: originals (== work when in place)
     void *codes;
     const double *outl;
     int64_t outl_cap;
@@ -384,12 +386,12 @@ __device__ __forceinline__ void process_warp(const SweepArgs &A, const CommitDev
         if (member) {
             if (DIR == HPEZ_COMPRESS) {
                 const double pred = predict(work, idx, coord, dims, estr, pr, s);
-                const double orig = ldv(work, idx);
+                const double orig = ldv((const T *)A.orig, idx);
                 double out;
                 const int64_t code = quantize_point<ROUND>(orig, pred, bound, two_e, inv_two_e, R, &out);
                 __stcg(codes + ci, (C)code);
                 esc = code == 0;
-                if (!esc) __stcg(work + idx, (T)out);
+                if (!esc || A.orig != A.work) __stcg(work + idx, (T)out);
                 if (STATS) {
                     const double err = fabs(__dsub_rn(orig, pred));
                     A.errbuf[ci] = err;
@@ -442,97 +444,6 @@ __device__ __forceinline__ void process_warp(const SweepArgs &A, const CommitDev
 // (0,1,2).  Geometry is held in registers and lattice indices advance
 // incrementally, so the per-point cost is the stencil, the quantizer and a
 // few integer operations.
-// 1-D row of family FAM at coordinate c (extent E, stride s, element step sE)
-// with every edge truncation of kernels.resolve_row (kernels.py:106-150)
-// written out: inter-level cubic rows try (-1,1,3), (-3,-1,1), (-1,1),
-// (-3,-1), (-1,); same-level rows (-2,-1,1,2), (-2,-1,1), (-2,-1); a
-// truncated 6-point natural row falls back to the 4-point not-a-knot row.
-// Edge rows of family FAM at coordinate c (extent E, stride s) over values
-// x[] already loaded at the family's nominal offsets (Fam<FAM>::u order),
-// with every truncation of kernels.resolve_row (kernels.py:106-150) written
-// out: inter-level cubic rows try (-1,1,3), (-3,-1,1), (-1,1), (-3,-1),
-// (-1,); same-level rows (-2,-1,1,2), (-2,-1,1), (-2,-1); a truncated
-// 6-point natural row falls back to the 4-point not-a-knot row.  Offsets
-// outside the grid were loaded from the target itself and are never used.
-template <int FAM>
-__device__ __forceinline__ double edge_row(const double (&x)[6], int c, int E, int s) {
-    const bool r1 = c + s <= E - 1;
-    if (FAM == FAM_LIN_I) return r1 ? DA(DM(0.5, x[0]), DM(0.5, x[1])) : DM(1.0, x[0]);
-    if (FAM == FAM_NAK_I || FAM == FAM_NAT_I) {
-        const double a = x[0], b = x[1], d = x[2], e = x[3];
-        const bool l3 = c >= 3 * s, r3 = c + 3 * s <= E - 1;
-        if (l3 && r3) {
-            if (FAM == FAM_NAK_I)
-                return DA(DA(DA(DM(-1.0 / 16, a), DM(9.0 / 16, b)), DM(9.0 / 16, d)), DM(-1.0 / 16, e));
-            return DA(DA(DA(DM(-3.0 / 40, a), DM(23.0 / 40, b)), DM(23.0 / 40, d)), DM(-3.0 / 40, e));
-        }
-        if (r3) return DA(DA(DM(3.0 / 8, b), DM(3.0 / 4, d)), DM(-1.0 / 8, e));
-        if (l3 && r1) return DA(DA(DM(-1.0 / 8, a), DM(3.0 / 4, b)), DM(3.0 / 8, d));
-        if (r1) return DA(DM(0.5, b), DM(0.5, d));
-        if (l3) return DA(DM(-0.5, a), DM(1.5, b));
-        return DM(1.0, b);
-    }
-    // same-level families: targets sit at >= 3s, so only the right side truncates
-    constexpr int o = FAM == FAM_NAT_S ? 1 : 0;
-    const double b = x[o], d = x[o + 1], e = x[o + 2], f = x[o + 3];
-    if (FAM == FAM_NAT_S && c + 3 * s <= E - 1)
-        return DA(DA(DA(DA(DA(DM(3.0 / 62, x[0]), DM(-18.0 / 62, b)), DM(46.0 / 62, d)), DM(46.0 / 62, e)),
-                     DM(-18.0 / 62, f)), DM(3.0 / 62, x[5]));
-    if (c + 2 * s <= E - 1) return DA(DA(DA(DM(-1.0 / 6, b), DM(4.0 / 6, d)), DM(4.0 / 6, e)), DM(-1.0 / 6, f));
-    if (r1) return DA(DA(DM(-1.0 / 3, b), DM(1.0, d)), DM(1.0 / 3, e));
-    return DA(DM(-1.0, b), DM(2.0, d));
-}
-
-// Stencil families at compile time: nominal offsets, interior test and the
-// full-row combination in the reference's left-to-right order.
-template <int FAM> struct Fam;
-template <> struct Fam<FAM_LIN_I> {
-    static constexpr int n = 2;
-    __device__ static constexpr int u(int i) { return i == 0 ? -1 : 1; }
-    __device__ static bool interior(int c, int E, int s) { return c + s <= E - 1; }
-    template <typename V> __device__ static double combine(const V (&v)[6]) {
-        return DA(DM(0.5, (double)v[0]), DM(0.5, (double)v[1]));
-    }
-};
-template <> struct Fam<FAM_NAK_I> {
-    static constexpr int n = 4;
-    __device__ static constexpr int u(int i) { return i == 0 ? -3 : i == 1 ? -1 : i == 2 ? 1 : 3; }
-    __device__ static bool interior(int c, int E, int s) { return c >= 3 * s && c + 3 * s <= E - 1; }
-    template <typename V> __device__ static double combine(const V (&v)[6]) {
-        return DA(DA(DA(DM(-1.0 / 16, (double)v[0]), DM(9.0 / 16, (double)v[1])), DM(9.0 / 16, (double)v[2])),
-                  DM(-1.0 / 16, (double)v[3]));
-    }
-};
-template <> struct Fam<FAM_NAT_I> {
-    static constexpr int n = 4;
-    __device__ static constexpr int u(int i) { return i == 0 ? -3 : i == 1 ? -1 : i == 2 ? 1 : 3; }
-    __device__ static bool interior(int c, int E, int s) { return c >= 3 * s && c + 3 * s <= E - 1; }
-    template <typename V> __device__ static double combine(const V (&v)[6]) {
-        return DA(DA(DA(DM(-3.0 / 40, (double)v[0]), DM(23.0 / 40, (double)v[1])), DM(23.0 / 40, (double)v[2])),
-                  DM(-3.0 / 40, (double)v[3]));
-    }
-};
-template <> struct Fam<FAM_NAK_S> {
-    static constexpr int n = 4;
-    __device__ static constexpr int u(int i) { return i == 0 ? -2 : i == 1 ? -1 : i == 2 ? 1 : 2; }
-    __device__ static bool interior(int c, int E, int s) { return c + 2 * s <= E - 1; }
-    template <typename V> __device__ static double combine(const V (&v)[6]) {
-        return DA(DA(DA(DM(-1.0 / 6, (double)v[0]), DM(4.0 / 6, (double)v[1])), DM(4.0 / 6, (double)v[2])),
-                  DM(-1.0 / 6, (double)v[3]));
-    }
-};
-template <> struct Fam<FAM_NAT_S> {
-    static constexpr int n = 6;
-    __device__ static constexpr int u(int i) {
-        return i == 0 ? -3 : i == 1 ? -2 : i == 2 ? -1 : i == 3 ? 1 : i == 4 ? 2 : 3;
-    }
-    __device__ static bool interior(int c, int E, int s) { return c + 3 * s <= E - 1; }
-    template <typename V> __device__ static double combine(const V (&v)[6]) {
-        return DA(DA(DA(DA(DA(DM(3.0 / 62, (double)v[0]), DM(-18.0 / 62, (double)v[1])), DM(46.0 / 62, (double)v[2])),
-                        DM(46.0 / 62, (double)v[3])), DM(-18.0 / 62, (double)v[4])), DM(3.0 / 62, (double)v[5]));
-    }
-};
-
 // grid axis of blend term t for a fast-path layout KIND
 template <int KIND> __device__ constexpr int kind_axis(int t) {
     return KIND < 3 ? KIND : KIND == 3 ? (t == 0 ? 0 : 1) : KIND == 4 ? (t == 0 ? 0 : 2) : KIND == 5 ? (t == 0 ? 1 : 2) : t;
@@ -561,6 +472,8 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
     const int32_t R32 = (int32_t)R;
     const double Rd = (double)R;
     T *__restrict__ work = (T *)A.work;
+    const T *__restrict__ origp = (const T *)A.orig;
+    const bool oop = A.orig != A.work;
     C *__restrict__ codes = (C *)A.codes;
     const int64_t cb = cm.code_base;
     C *__restrict__ cptr = codes + cb + p0 + lane;  // this lane's code slot, +32 per iteration
@@ -615,8 +528,8 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
             kA = (int64_t)cptr[0];
             kB = (int64_t)cptr[32];
         } else {
-            oA = work[iA];
-            oB = work[iB];
+            oA = origp[iA];
+            oB = origp[iB];
         }
 #pragma unroll
         for (int t = 0; t < NAX; t++) {
@@ -640,11 +553,11 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
             int32_t c = quantize_point<ROUND>((double)oA, predA, bound, two_e, inv_two_e, Rd, R32, &out);
             cptr[0] = (C)c;
             eA = c == 0;
-            if (!eA) work[iA] = (T)out;
+            if (!eA || oop) work[iA] = (T)out;
             c = quantize_point<ROUND>((double)oB, predB, bound, two_e, inv_two_e, Rd, R32, &out);
             cptr[32] = (C)c;
             eB = c == 0;
-            if (!eB) work[iB] = (T)out;
+            if (!eB || oop) work[iB] = (T)out;
         } else {
             eA = kA == 0;
             eB = kB == 0;
@@ -693,7 +606,7 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
             T v[NAX][6];
             T o = T(0);
             if (DIR == HPEZ_DECOMPRESS) code = (int64_t)*cptr;
-            else o = work[idx];
+            else o = origp[idx];
             double pt[NAX];
             if (warp_interior) {
 #pragma unroll
@@ -732,7 +645,7 @@ __device__ __forceinline__ void process_fast(const SweepArgs &A, const CommitDev
                 const int32_t c = quantize_point<ROUND>(origv, pred, bound, two_e, inv_two_e, Rd, R32, &out);
                 *cptr = (C)c;
                 esc = c == 0;
-                if (!esc) work[idx] = (T)out;
+                if (!esc || oop) work[idx] = (T)out;
             } else if (code != 0) {
                 work[idx] = (T)dequantize_point<ROUND>(pred, code, two_e, R);
             } else {
@@ -988,7 +901,7 @@ __global__ void __launch_bounds__(256) gather_outliers_kernel(const __grid_const
     const bool has = e0 + lane < n_entries && A.esc_cnt[e0 + lane] != 0;
     uint32_t todo = __ballot_sync(0xffffffffu, has);
     const GridDev &g = A.g;
-    const T *work = (const T *)A.work;
+    const T *work = (const T *)A.orig;  // escaped points hold their originals in both buffers
     const C *codes = (const C *)A.codes;
     while (todo) {
         const int k = __ffs(todo) - 1;
@@ -1164,6 +1077,23 @@ __global__ void commit_ranges_kernel(const CommitDev *commits, int nc, const int
     cn[c] = n;
 }
 
+// Out-of-place compress: copy the anchor lattice (multiples of A on every
+// non-frozen axis, plan.py:142-161) from the originals into work.
+__global__ void copy_anchors_kernel(GridDev g, uint32_t A, uint32_t frozen, int64_t na, const char *orig, char *work,
+                                    int esz) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= na) return;
+    int64_t idx = 0;
+    for (int a = g.rank - 1; a >= 0; a--) {
+        const int64_t n = (frozen >> a & 1) ? g.dims[a] : (g.dims[a] + A - 1) / A;
+        const int64_t j = i % n;
+        i /= n;
+        idx += ((frozen >> a & 1) ? j : j * A) * g.estr[a];
+    }
+    if (esz == 4) ((float *)work)[idx] = ((const float *)orig)[idx];
+    else ((double *)work)[idx] = ((const double *)orig)[idx];
+}
+
 // ----------------------------------------------------------- host plan --
 struct Cfg {
     int spline = 0, same = 0, md = 0;
@@ -1235,6 +1165,9 @@ struct Plan {
     std::vector<uint32_t> c_vmask, c_reads;
     std::vector<int32_t> wn;   // member count per (item, warp); mixed filled on device
     std::vector<int32_t> mixed_items;
+    int32_t c_tile = 0;             // commits [c_tile, n) run as tiled levels (tile.cu)
+    std::vector<TilePlan> tiles;    // one per tiled level
+    void *d_orig_scratch = nullptr; // originals copy for in-place compress with tiled levels
 
     // device
     CommitDev *d_commits = nullptr;
@@ -1265,7 +1198,7 @@ struct Plan {
         void *ptrs[] = {d_prof, d_commits, d_item_commit, d_flow_order, d_dep_off, d_coarse_pairs, d_coarse_groups,
                         d_dep_rng, d_wbase, d_wn, d_esc_cnt, d_esc_off,
                         d_scan_tmp, d_total, d_done, d_counters, d_tags, d_slots, d_table,
-                        d_mixed_items, d_cbase, d_cn, d_clevel, d_errbuf, d_csum};
+                        d_mixed_items, d_cbase, d_cn, d_clevel, d_errbuf, d_csum, d_orig_scratch};
         for (void *p : ptrs)
             if (p) cudaFree(p);
     }
@@ -1489,7 +1422,9 @@ struct Plan {
             level_codes.push_back(code_pos);
         }
         num_codes = code_pos;
+        choose_tiles(false);
         build_items();
+        choose_tiles(true);
         return HPEZ_OK;
     }
 
@@ -1618,9 +1553,9 @@ struct Plan {
         {
             int c = 0;
             uint64_t pts = 0;
-            while (c < nc) {
+            while (c < c_tile) {
                 int e = c;
-                while (e < nc && commits[e].level == commits[c].level) pts += commits[e++].npos;
+                while (e < c_tile && commits[e].level == commits[c].level) pts += commits[e++].npos;
                 if (pts > coarse_max || (size_t)e * sizeof(CommitDev) > 200 * 1024) break;
                 c = e;
             }
@@ -1715,7 +1650,7 @@ struct Plan {
                 }
                 if (cm.kind != COMMIT_UNIFORM) mixed_items.push_back(gi);
                 dep_off[gi] = (int32_t)dep_rng.size();
-                if (ci >= c_coarse) {
+                if (ci >= c_coarse && ci < c_tile) {
                     for (int d : preds[ci])
                         if (d >= c_coarse) dep_rng.push_back(dep_interval(cm, it, commits[d]));
                     const int64_t U = (int64_t)cm.npos / cm.cnt[0];
@@ -1772,7 +1707,7 @@ struct Plan {
         first_flow_item = 0;
         flow_grid = std::max(1, (int)flow_order.size());  // capped by occupancy at launch
         coarse_fast = flow_fast = true;
-        for (int ci = 0; ci < nc; ci++) {
+        for (int ci = 0; ci < c_tile; ci++) {
             CommitDev &cm = commits[ci];
             cm.fast_id = fast_id_of(cm);
             bool &f = ci < c_coarse ? coarse_fast : flow_fast;
@@ -1781,6 +1716,48 @@ struct Plan {
         if (getenv("HPEZ_COARSE_GENERIC")) coarse_fast = false;
     }
     int d_rank() const { return d.rank; }
+
+    // Finest levels that run as shared-memory tiled launches (tile.cu):
+    // rank-3 f32 grids with u16 codes, no stats, uniform commits, at least
+    // HPEZ_TILE_MIN points (default 200k).  `final` builds the real plans
+    // once build_items has assigned the (item, warp) stream bookkeeping.
+    void choose_tiles(bool final) {
+        const int nc = (int)commits.size();
+        if (final) {
+            tiles.clear();
+            for (int c = c_tile; c < nc;) {
+                int e = c;
+                while (e < nc && commits[e].level == commits[c].level) e++;
+                TilePlan tp;
+                tile_plan_build(g, &commits[c], e - c, num_codes, &tp);
+                tiles.push_back(tp);
+                c = e;
+            }
+            return;
+        }
+        c_tile = nc;
+        // opt-in (HPEZ_TILE=1): measured slower than the flow kernel on cfg2
+        // so far (profiles/); kept parity-green for the tiling work ahead
+        const char *ev = getenv("HPEZ_TILE");
+        if (!ev || atoi(ev) == 0) return;
+        if (d.rank != 3 || d.with_stats || d.work_dtype != HPEZ_WORK_F32 || d.rounding != HPEZ_ROUND_F32 ||
+            d.code_dtype != HPEZ_CODES_U16 || d.frozen_mask)
+            return;
+        int64_t min_pts = 200000;
+        if (const char *m = getenv("HPEZ_TILE_MIN")) min_pts = atoll(m);
+        int c = nc;
+        while (c > 0) {
+            int b = c;
+            const int lvl = commits[c - 1].level;
+            int64_t pts = 0;
+            while (b > 0 && commits[b - 1].level == lvl) pts += commits[--b].npos;
+            if (pts < min_pts) break;
+            TilePlan tp;
+            if (!tile_plan_build(g, &commits[b], c - b, num_codes, &tp)) break;
+            c = b;
+        }
+        c_tile = c;
+    }
 };
 
 template <typename T>
@@ -1985,6 +1962,7 @@ int32_t hpez_plan_num_launches(hpez_plan plan) {
     int n = 0;
     if (!p.coarse_groups.empty()) n++;
     if (!p.flow_order.empty()) n++;
+    n += (int)p.tiles.size();
     n += 3;  // escape scan (3 kernels)
     n += 1;  // escape count pre-pass (decompress) or outlier gather (compress)
     if (p.d.with_stats && p.d.direction == HPEZ_COMPRESS) n += 2;
@@ -2034,11 +2012,35 @@ int hpez_set_device(int32_t device) { return cuda_status(cudaSetDevice(device));
 
 const char *hpez_build_info(void) { return "libhpez_b200 sm_100a f64 -fmad=false"; }
 
-int hpez_sweep_run(hpez_plan plan, void *work, void *codes, int64_t codes_avail, double *outliers, int64_t outl_cap,
-                   double *stat_err_sum, int64_t *stat_count, double *stat_dense, void *stream) {
+static int sweep_run(hpez_plan plan, const void *orig, void *work, void *codes, int64_t codes_avail, double *outliers,
+                     int64_t outl_cap, double *stat_err_sum, int64_t *stat_count, double *stat_dense, void *stream) {
     if (!plan || !work) return HPEZ_BAD_ARGUMENT;
     Plan &p = plan->p;
     cudaStream_t st = (cudaStream_t)stream;
+    const size_t esz = p.d.work_dtype == HPEZ_WORK_F32 ? 4 : 8;
+    if (p.d.direction != HPEZ_COMPRESS || !orig) orig = work;
+    if (orig != work) {
+        // anchors: the lattice no commit covers (plan.py:142-161)
+        if (p.levels.empty() || p.d.with_stats) return HPEZ_BAD_ARGUMENT;
+        const int64_t A = 2 * (int64_t)p.levels[0].stride;
+        int64_t na = 1;
+        for (int a = 0; a < p.d.rank; a++)
+            na *= (p.d.frozen_mask >> a & 1) ? p.g.dims[a] : (p.g.dims[a] + A - 1) / A;
+        if (na + p.num_codes != p.g.npts) return HPEZ_BAD_ARGUMENT;
+        const int64_t thr = std::max<int64_t>(na, 1);
+        copy_anchors_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(p.g, (uint32_t)A, p.d.frozen_mask, na,
+                                                                           (const char *)orig, (char *)work, (int)esz);
+    } else if (p.d.direction == HPEZ_COMPRESS && !p.tiles.empty()) {
+        // tiled levels recompute halo points from originals that a neighbour
+        // may already have overwritten in place: keep a copy
+        if (!p.d_orig_scratch) {
+            cudaError_t e = cudaMalloc(&p.d_orig_scratch, (size_t)p.g.npts * esz);
+            if (e) return cuda_status(e);
+        }
+        cudaError_t e = cudaMemcpyAsync(p.d_orig_scratch, work, (size_t)p.g.npts * esz, cudaMemcpyDeviceToDevice, st);
+        if (e) return cuda_status(e);
+        orig = p.d_orig_scratch;
+    }
     if (p.d.direction == HPEZ_DECOMPRESS && codes_avail < p.num_codes) return HPEZ_CORRUPT_STREAM;
     if (p.num_codes > 0 && !codes) return HPEZ_BAD_ARGUMENT;
     const bool stats = p.d.with_stats && p.d.direction == HPEZ_COMPRESS;
@@ -2059,6 +2061,7 @@ int hpez_sweep_run(hpez_plan plan, void *work, void *codes, int64_t codes_avail,
     if (e) return cuda_status(e);
     SweepArgs A = base_args(p);
     A.work = work;
+    A.orig = orig;
     A.codes = codes;
     A.outl = outliers;
     A.outl_cap = outliers ? outl_cap : 0;
@@ -2111,6 +2114,18 @@ int hpez_sweep_run(hpez_plan plan, void *work, void *codes, int64_t codes_avail,
     }
     e = cudaGetLastError();
     if (e) return cuda_status(e);
+    if (!p.tiles.empty()) {
+        const int64_t e0 = (int64_t)p.commits[p.c_tile].item_base * kItemWarps;
+        if (p.d.direction == HPEZ_COMPRESS) {
+            e = cudaMemsetAsync(p.d_esc_cnt + e0, 0, (size_t)(ne - e0) * sizeof(uint32_t), st);
+            if (e) return cuda_status(e);
+        }
+        TileRun tr{orig, work, codes, outliers, A.outl_cap, p.d_esc_cnt, p.d_esc_off, p.d_counters + 1};
+        for (const TilePlan &tp : p.tiles) {
+            e = tile_plan_launch(tp, p.d.direction, tr, st);
+            if (e) return cuda_status(e);
+        }
+    }
     if (p.d.direction == HPEZ_COMPRESS) {
         exclusive_scan(p.d_esc_cnt, ne, p.d_esc_off, p.d_scan_tmp, p.d_total, st);
         const int64_t thr = (ne + 31) / 32 * 32;
@@ -2129,6 +2144,31 @@ int hpez_sweep_run(hpez_plan plan, void *work, void *codes, int64_t codes_avail,
     e = cudaGetLastError();
     if (e) return cuda_status(e);
     p.outl_cap_last = A.outl_cap;
+    return HPEZ_OK;
+}
+
+int hpez_sweep_run(hpez_plan plan, void *work, void *codes, int64_t codes_avail, double *outliers, int64_t outl_cap,
+                   double *stat_err_sum, int64_t *stat_count, double *stat_dense, void *stream) {
+    return sweep_run(plan, nullptr, work, codes, codes_avail, outliers, outl_cap, stat_err_sum, stat_count, stat_dense,
+                     stream);
+}
+
+int hpez_sweep_run_from(hpez_plan plan, const void *orig, void *work, void *codes, int64_t codes_avail,
+                        double *outliers, int64_t outl_cap, void *stream) {
+    if (!orig) return HPEZ_BAD_ARGUMENT;
+    return sweep_run(plan, orig, work, codes, codes_avail, outliers, outl_cap, nullptr, nullptr, nullptr, stream);
+}
+
+int hpez_plan_tile_info(hpez_plan plan, int64_t *out, int32_t cap) {
+    if (!plan || !out || cap < 1) return HPEZ_BAD_ARGUMENT;
+    const Plan &p = plan->p;
+    out[0] = (int64_t)p.tiles.size();
+    int k = 1, c = p.c_tile;
+    for (const TilePlan &t : p.tiles) {
+        const int64_t v[8] = {c, t.grid, t.threads, (int64_t)t.smem, t.d.TY, t.d.TX, t.d.ZC, t.d.n_iv};
+        for (int i = 0; i < 8 && k < cap; i++) out[k++] = v[i];
+        c += t.d.n_commits;
+    }
     return HPEZ_OK;
 }
 

@@ -1,0 +1,82 @@
+// tile.h -- shared-memory tiled level sweep (tile.cu), host interface used by
+// the sweep planner (sweep.cu).
+//
+// One launch runs one whole level of a rank-3 uniform sweep
+// (interp._LevelRunner.run_level, interp.py:415-433, with every class on the
+// uniform path, interp.py:322-341).  The level's points form the stride-s
+// sublattice; CTAs own (y, x) tiles x z-chunks of it, stream the chunk plane by
+// plane through an f64 ring of planes in shared memory and recompute the
+// halo points their owned points depend on, so no CTA ever waits on another.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace hpez {
+
+constexpr int kTileMaxCommits = 16;
+constexpr int kTileMaxTasks = 64;
+constexpr int kTileMaxIntervals = 32;
+constexpr int kTileEvenSlots = 8;  // ring slots (see slot_off in tile.cu)
+constexpr int kTileOddSlots = 5;
+
+struct TileCommit {
+    int32_t v, split, phase, odd;  // class mask, split axis (-1), phase, axis 0 in v
+    int32_t st[3], sh[3], cnt[3];  // lattice in sublattice units: j = st + (i << sh)
+    int32_t box[4];                // compute-box extension beyond the owned tile: ylo, yhi, xlo, xhi
+    int32_t item_base, p_item, pw; // stream bookkeeping (escape counts per (item, warp))
+    int32_t fam, nax, kind;        // predictor: stencil family, 1 (1-D) .. 3 axes, layout (tk_axis)
+    int32_t pad;
+    int32_t axes[3];
+    double w[3];                   // MD blend weights (nax >= 2)
+    int64_t code_base;
+};
+
+struct TileDesc {
+    int32_t L[3];                  // sublattice extents
+    int32_t s;
+    int32_t E0, E1;                // grid element strides of axes 0 and 1
+    int32_t TY, TX, ZC;            // tile (owned) sizes
+    int32_t tiles_y, tiles_x, chunks_z;
+    int32_t HYe, HXe, HYo, HXo;    // ring halos (even / odd planes); HX even
+    int32_t RYe, RXe, RYo, RXo;    // ring plane dims
+    int32_t n_commits, n_iv;
+    int32_t R;
+    int64_t n_codes;               // whole code stream (bounds the aligned code-word loads)
+    double bound, two_e, inv_two_e;
+    int32_t iv_off[kTileMaxIntervals + 1];
+    int8_t task_sel[kTileMaxTasks];   // 0: even plane 4m, 1: 4m+2, 2: odd 4m-3, 3: odd 4m-5
+    int8_t task_c[kTileMaxTasks];
+    int8_t lut[64];                   // ((z&3)<<4)|((y&3)<<2)|(x&3) -> commit, -1 = coarse
+    TileCommit c[kTileMaxCommits];
+};
+
+struct TileRun {
+    const void *orig;     // compress: originals (read-only)
+    void *work;           // reconstruction (coarse points read, level points written)
+    void *codes;
+    const double *outl;   // decompress outliers
+    int64_t outl_cap;
+    uint32_t *esc_cnt;    // per (item, warp) escapes (compress: incremented)
+    const int64_t *esc_off;  // per (item, warp) first outlier rank (decompress)
+    int32_t *flags;
+};
+
+struct TilePlan {
+    TileDesc d;
+    int grid = 0;
+    int threads = 0;
+    size_t smem = 0;
+};
+
+// Builds the tiled plan of one level from its commit descriptors (reference
+// order).  Returns false when the level is not eligible (rank != 3, frozen or
+// mixed commits, > kTileMaxCommits commits, ring larger than shared memory).
+bool tile_plan_build(const GridDev &g, const CommitDev *cms, int n, int64_t n_codes, TilePlan *out);
+
+// Launches one level (f32 work, u16 codes).  dir = HPEZ_COMPRESS / HPEZ_DECOMPRESS.
+cudaError_t tile_plan_launch(const TilePlan &p, int dir, const TileRun &r, cudaStream_t st);
+
+}  // namespace hpez

@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import collections
 import ctypes
+import os
 import hashlib
 
 import numpy as np
@@ -109,6 +110,7 @@ class SweepPlan:
 
 _PLANS: "collections.OrderedDict[bytes, SweepPlan]" = collections.OrderedDict()
 _PLAN_CAP = 48
+_PLAN_ENV = ("HPEZ_TILE", "HPEZ_TILE_MIN", "HPEZ_TILE_TY", "HPEZ_TILE_TX", "HPEZ_TILE_ZC", "HPEZ_TILE_NT")
 
 
 def _level_array(levels, rank):
@@ -168,6 +170,8 @@ def get_plan(dims, levels, *, direction, radius, frozen_axes=(), md_alpha=None,
     key.update(bytes(lv))
     key.update(b"" if md is None else md.tobytes())
     key.update(b"" if tbl is None else tbl.tobytes())
+    # planner knobs (tiled levels) read by the library at plan creation
+    key.update(repr([os.environ.get(v) for v in _PLAN_ENV]).encode())
     # a plan owns its run scratch (escape counts, flags, counters), so each
     # (device, stream) pair gets its own instance: sweeps on different
     # streams may run concurrently
@@ -194,7 +198,7 @@ def torch_code_dtype(code_dtype: int):
 
 def run_levels_device(work, levels, *, direction, radius, frozen_axes=(), md_alpha=None,
                       rounding=ROUND_NONE, block_size=0, block_table=None, codes=None,
-                      outliers=None, stats=None, sync=True):
+                      outliers=None, stats=None, sync=True, orig=None):
     """Device-resident sweep.
 
     ``work``: contiguous CUDA tensor (float32 storage requires every value,
@@ -203,6 +207,9 @@ def run_levels_device(work, levels, *, direction, radius, frozen_axes=(), md_alp
     u16 when radius <= 32768); decompress consumes ``codes`` / ``outliers``
     device tensors and returns the number of outliers used.  ``stats`` is a
     dict of device tensors ``err_sum``/``count``/``dense`` (optional).
+    ``orig`` (compress, no stats): read the originals from this tensor instead
+    and write the anchors plus every reconstruction into ``work`` -- the
+    pipeline's ``work = f64(grid)`` copy (pipeline.py:82) folded into the sweep.
     """
     if direction not in ("compress", "decompress"):
         raise ValueError(f"bad direction {direction!r}")
@@ -228,9 +235,16 @@ def run_levels_device(work, levels, *, direction, radius, frozen_axes=(), md_alp
         es = cnt = dense = None
         if stats is not None:
             es, cnt, dense = stats.get("err_sum"), stats.get("count"), stats.get("dense")
-        check(L.hpez_sweep_run(plan.handle, ptr(work), ptr(codes), codes.numel(), ptr(outliers),
-                               outliers.numel(), ptr(es), ptr(cnt), ptr(dense), st),
-              "hpez_sweep_run")
+        if orig is not None:
+            if stats is not None or orig.shape != work.shape or orig.dtype != work.dtype \
+                    or not orig.is_cuda or not orig.is_contiguous():
+                raise ValueError("orig must be a contiguous CUDA tensor like work (no stats)")
+            check(L.hpez_sweep_run_from(plan.handle, ptr(orig), ptr(work), ptr(codes), codes.numel(),
+                                        ptr(outliers), outliers.numel(), st), "hpez_sweep_run_from")
+        else:
+            check(L.hpez_sweep_run(plan.handle, ptr(work), ptr(codes), codes.numel(), ptr(outliers),
+                                   outliers.numel(), ptr(es), ptr(cnt), ptr(dense), st),
+                  "hpez_sweep_run")
         n_out = ctypes.c_int64(0)
         if sync:
             check(L.hpez_sweep_finish(plan.handle, st, ctypes.byref(n_out)), "hpez_sweep_finish")

@@ -21,14 +21,14 @@ def flush_op(v):
     elif FL == "read": flush.fill_(v); torch.cuda.synchronize(); flush.sum()
     elif FL == "readonly": flush.sum()
 tc, td = [], []
-for it in range(8):
+for it in range(int(os.environ.get('ITERS', 8))):
     w.copy_(orig); flush_op(1.0)
     e0, e1, e2, e3 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    e0.record(); codes, outl, n = run_levels_device(w, lv, direction="compress", sync=False, **kw); e1.record()
+    e0.record(); codes, outl, n = run_levels_device(w, lv, direction="compress", sync=False, orig=orig, **kw); e1.record()
     back.copy_(a0); flush_op(2.0)
     e2.record(); run_levels_device(back, lv, direction="decompress", codes=codes, outliers=outl, sync=False, **kw); e3.record()
     torch.cuda.synchronize()
-    if it >= 3:
+    if it >= min(3, int(os.environ.get('ITERS', 8)) - 1):
         tc.append(e0.elapsed_time(e1)); td.append(e2.elapsed_time(e3))
 assert os.environ.get('HPEZ_DEBUG_NODEPS') or torch.equal(back, w)
 print(json.dumps({"env": {k: v for k, v in os.environ.items() if k.startswith("HPEZ_")}, "compress_ms": round(float(np.median(tc)), 4), "decompress_ms": round(float(np.median(td)), 4)}))
