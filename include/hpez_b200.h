@@ -165,7 +165,9 @@ int hpez_plan_level_codes(hpez_plan plan, int64_t *out);
 
 /* Plan diagnostics (12 int64): item counts, schedule flags and, when the
  * environment variable HPEZ_PROFILE is set at plan creation, the flow
- * kernel's clock64 phase counters (grab, wait, work, units). */
+ * kernel's clock64 phase counters (grab, wait, work, units).  out[6]: bit 0
+ * fast coarse cluster path, bit 1 coarse levels in distributed shared
+ * memory (coarse.cu). */
 int hpez_plan_info(hpez_plan plan, int64_t *out);
 
 /* HPEZ_PROFILE plans only: out[0..24) per-level (first item start, last

@@ -1206,6 +1206,9 @@ struct Plan {
     int32_t c_tile = 0;             // commits [c_tile, n) run as tiled levels (tile.cu)
     std::vector<TilePlan> tiles;    // one per tiled level
     void *d_orig_scratch = nullptr; // originals copy for in-place compress with tiled levels
+    std::vector<int> coarse_group;  // (level, depth) group of each coarse commit
+    CoarsePlan cplan;               // coarse levels in distributed shared memory (coarse.cu)
+    bool coarse_dsmem = false;
 
     // device
     CommitDev *d_commits = nullptr;
@@ -1463,6 +1466,11 @@ struct Plan {
         choose_tiles(false);
         build_items();
         choose_tiles(true);
+        coarse_dsmem = false;
+        const char *cd = getenv("HPEZ_COARSE_DSMEM");
+        if (c_coarse > 0 && !(cd && atoi(cd) == 0) && d.rank == 3 && !d.with_stats && !d.frozen_mask &&
+            d.work_dtype == HPEZ_WORK_F32 && d.rounding == HPEZ_ROUND_F32 && d.code_dtype == HPEZ_CODES_U16)
+            coarse_dsmem = coarse_dsmem_build(g, commits.data(), coarse_group.data(), c_coarse, num_codes, &cplan);
         return HPEZ_OK;
     }
 
@@ -1648,6 +1656,7 @@ struct Plan {
         // coarse schedule: (level, depth) groups of (commit, item) pairs
         coarse_pairs.clear();
         coarse_groups.clear();
+        coarse_group.assign(c_coarse, 0);
         for (int c = 0; c < c_coarse;) {
             int e = c;
             while (e < c_coarse && commits[e].level == commits[c].level) e++;
@@ -1655,6 +1664,8 @@ struct Plan {
             for (int k = c; k < e; k++) maxd = std::max(maxd, depth[k]);
             for (int dd = 0; dd <= maxd; dd++) {
                 const int g0 = (int)coarse_pairs.size() / 2;
+                for (int k = c; k < e; k++)
+                    if (depth[k] == dd) coarse_group[k] = (int)coarse_groups.size() / 2;
                 for (int k = c; k < e; k++)
                     if (depth[k] == dd)
                         for (int it = 0; it < commits[k].n_items; it++) {
@@ -2029,7 +2040,7 @@ int hpez_plan_info(hpez_plan plan, int64_t *out) {
     out[3] = (int64_t)p.coarse_groups.size() / 2;
     out[4] = p.diag_order;
     out[5] = p.flow_fast;
-    out[6] = p.coarse_fast;
+    out[6] = p.coarse_fast + 2 * p.coarse_dsmem;  // bit 1: coarse levels in distributed shared memory
     out[7] = (int64_t)p.dep_rng.size();
     for (int i = 8; i < 12; i++) out[i] = -1;
     if (p.d_prof) {
@@ -2117,7 +2128,19 @@ static int sweep_run(hpez_plan plan, const void *orig, void *work, void *codes, 
                                                                              ne, p.d_esc_cnt);
         exclusive_scan(p.d_esc_cnt, ne, p.d_esc_off, p.d_scan_tmp, p.d_total, st);
     }
-    if (!p.coarse_groups.empty()) {
+    if (p.coarse_dsmem) {
+        if (p.d.direction == HPEZ_COMPRESS && p.c_coarse < (int)p.commits.size()) {
+            const int64_t e1 = (int64_t)p.commits[p.c_coarse].item_base * kItemWarps;
+            e = cudaMemsetAsync(p.d_esc_cnt, 0, (size_t)e1 * sizeof(uint32_t), st);
+            if (e) return cuda_status(e);
+        } else if (p.d.direction == HPEZ_COMPRESS) {
+            e = cudaMemsetAsync(p.d_esc_cnt, 0, (size_t)ne * sizeof(uint32_t), st);
+            if (e) return cuda_status(e);
+        }
+        TileRun cr{orig, work, codes, outliers, A.outl_cap, p.d_esc_cnt, p.d_esc_off, p.d_counters + 1};
+        e = coarse_dsmem_launch(p.cplan, p.d.direction, cr, st);
+        if (e) return cuda_status(e);
+    } else if (!p.coarse_groups.empty()) {
         sweep_fn f = (p.coarse_fast && ks.coarse_fast) ? ks.coarse_fast : ks.coarse;
         const size_t smem = (size_t)p.c_coarse * sizeof(CommitDev);
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1));

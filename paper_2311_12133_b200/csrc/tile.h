@@ -79,4 +79,51 @@ bool tile_plan_build(const GridDev &g, const CommitDev *cms, int n, int64_t n_co
 // Launches one level (f32 work, u16 codes).  dir = HPEZ_COMPRESS / HPEZ_DECOMPRESS.
 cudaError_t tile_plan_launch(const TilePlan &p, int dir, const TileRun &r, cudaStream_t st);
 
+
+// ---------------------------------------------------------------- coarse --
+// Leading levels held in the distributed shared memory of one cluster
+// (coarse.cu).  Lattices are in units of the stride-Sc sublattice.
+constexpr int kCoarseMaxCommits = 96;
+constexpr int kCoarseMaxGroups = 64;
+constexpr int kCoarseMaxLevels = 6;
+constexpr int kCoarseDsmemThreads = 1024;
+
+struct CoarseCommit {
+    int32_t st[3], sp[3], cnt[3];  // j = st + i * sp (sublattice units)
+    int32_t sh[3];                 // log2(sp)
+    int32_t s;                     // level stride (sublattice units)
+    FastDiv fd_row, fd_x;          // division by cnt[1]*cnt[2] and by cnt[2]
+    int32_t kind, fam;             // predictor layout (tk_axis) and family
+    int32_t item_base, p_item, pw;
+    double w[3];
+    double bound, two_e, inv_two_e;
+    int64_t code_base;
+};
+
+struct CoarseDesc {
+    int32_t L[3];
+    int32_t Sc, E0, E1, P;         // sublattice stride, grid strides, planes per CTA
+    int32_t R;
+    int32_t n_commits, n_groups, n_levels;
+    int64_t n_codes;
+    int32_t grp_off[kCoarseMaxGroups + 1];
+    int32_t lvl_s[kCoarseMaxLevels], lvl_sh[kCoarseMaxLevels];
+    FastDiv fd_plane, fd_x;         // division by L1*L2 and by L2
+    int8_t lut[kCoarseMaxLevels][64];
+    CoarseCommit c[kCoarseMaxCommits];
+};
+
+struct CoarsePlan {
+    CoarseDesc d;
+    int ncta = 0;
+    size_t smem = 0;
+};
+
+// group[i]: (level, DAG depth) group of commit i (non-decreasing runs define
+// the cluster barriers).  False when not eligible (rank != 3, mixed
+// commits, too many commits/groups, slab above shared memory).
+bool coarse_dsmem_build(const GridDev &g, const CommitDev *cms, const int *group, int n, int64_t n_codes,
+                        CoarsePlan *out);
+cudaError_t coarse_dsmem_launch(const CoarsePlan &p, int dir, const TileRun &r, cudaStream_t st);
+
 }  // namespace hpez

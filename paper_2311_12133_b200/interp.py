@@ -110,7 +110,8 @@ class SweepPlan:
 
 _PLANS: "collections.OrderedDict[bytes, SweepPlan]" = collections.OrderedDict()
 _PLAN_CAP = 48
-_PLAN_ENV = ("HPEZ_TILE", "HPEZ_TILE_MIN", "HPEZ_TILE_TY", "HPEZ_TILE_TX", "HPEZ_TILE_ZC", "HPEZ_TILE_NT")
+_PLAN_ENV = ("HPEZ_TILE", "HPEZ_TILE_MIN", "HPEZ_TILE_TY", "HPEZ_TILE_TX", "HPEZ_TILE_ZC", "HPEZ_TILE_NT",
+             "HPEZ_COARSE_MAX", "HPEZ_COARSE_CLUSTER", "HPEZ_COARSE_DSMEM")
 
 
 def _level_array(levels, rank):
