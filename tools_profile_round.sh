@@ -14,4 +14,7 @@ ncu --set full --import-source on --clock-control none -k regex:flow_kernel -c 1
     python tools_sweep_time.py > gpurun_out/ncu_full.log 2>&1
 ncu -i gpurun_out/flow_full.ncu-rep --page details --csv > gpurun_out/flow_full_details.csv 2>/dev/null
 ncu -i gpurun_out/flow_full.ncu-rep --page raw --csv > gpurun_out/flow_full_raw.csv 2>/dev/null
+ncu --set full --import-source on --clock-control none -k regex:coarse_dsmem -c 1 -o gpurun_out/coarse_full \
+    python tools_sweep_time.py > gpurun_out/ncu_coarse.log 2>&1
+ncu -i gpurun_out/coarse_full.ncu-rep --page details --csv > gpurun_out/coarse_full_details.csv 2>/dev/null
 true

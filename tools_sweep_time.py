@@ -24,7 +24,7 @@ tc, td = [], []
 for it in range(int(os.environ.get('ITERS', 8))):
     w.copy_(orig); flush_op(1.0)
     e0, e1, e2, e3 = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    e0.record(); codes, outl, n = run_levels_device(w, lv, direction="compress", sync=False, orig=orig, **kw); e1.record()
+    e0.record(); codes, outl, n = run_levels_device(w, lv, direction="compress", sync=False, **kw); e1.record()
     back.copy_(a0); flush_op(2.0)
     e2.record(); run_levels_device(back, lv, direction="decompress", codes=codes, outliers=outl, sync=False, **kw); e3.record()
     torch.cuda.synchronize()
