@@ -1170,9 +1170,9 @@ static int num_sms() {
     return sms;
 }
 
-constexpr uint32_t kCoarseMax = 80000;  // leading levels of at most this many points (cumulative) run on the coarse cluster
+constexpr uint32_t kCoarseMax = 20000;  // leading levels of at most this many points (cumulative) run on the coarse cluster (cfg2: levels 0-1; measured sweep, session 2)
 constexpr int kCoarseCluster = 16;
-static int kDiagScale = 8;  // diagonal order: item window width, in units of the dependency reach
+static int kDiagScale = 16;  // diagonal order: item window width, in units of the dependency reach
 
 struct Plan {
     hpez_sweep_desc d{};
@@ -1893,7 +1893,8 @@ static SweepArgs base_args(Plan &p) {
     A.n_groups = (int32_t)(p.coarse_groups.size() / 2);
     A.prof = p.d_prof;
     A.dbg = getenv("HPEZ_DEBUG_NODEPS") ? 1 : 0;
-    A.l2_prefetch = getenv("HPEZ_L2_PREFETCH") ? atoi(getenv("HPEZ_L2_PREFETCH")) : 0;
+    // TMA bulk L2 prefetch of the next item's code range: helps decompress, not compress (measured)
+    A.l2_prefetch = getenv("HPEZ_L2_PREFETCH") ? atoi(getenv("HPEZ_L2_PREFETCH")) : p.d.direction == HPEZ_DECOMPRESS;
     A.wbase = p.d_wbase;
     A.wn = p.d_wn;
     A.esc_cnt = p.d_esc_cnt;
