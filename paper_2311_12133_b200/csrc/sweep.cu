@@ -933,6 +933,54 @@ __global__ void __launch_bounds__(256) count_zero_kernel(const C *__restrict__ c
     if (lane == 0) cnt[e] = z;
 }
 
+
+// Decompress pre-pass for u16 streams as a pure streaming read: CTA b owns
+// entries [b*kZeroEpb, ...) whose code ranges are contiguous in the stream,
+// reads them with aligned 16-byte loads, tests eight codes at once and only
+// for a chunk holding a zero code searches the entry it belongs to.
+constexpr int kZeroEpb = 32;
+__global__ void __launch_bounds__(256) count_zero_stream_kernel(const uint16_t *__restrict__ codes,
+                                                                const int64_t *__restrict__ wbase,
+                                                                const int32_t *__restrict__ wn, int64_t n_entries,
+                                                                uint32_t *__restrict__ cnt) {
+    __shared__ int64_t s_base[kZeroEpb + 1];
+    __shared__ uint32_t s_cnt[kZeroEpb];
+    const int64_t e0 = (int64_t)blockIdx.x * kZeroEpb;
+    const int ne = (int)min((int64_t)kZeroEpb, n_entries - e0);
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+        s_base[i] = wbase[e0 + i];
+        s_cnt[i] = 0;
+    }
+    if (threadIdx.x == 0) s_base[ne] = wbase[e0 + ne - 1] + wn[e0 + ne - 1];
+    __syncthreads();
+    const int64_t c0 = s_base[0], c1 = s_base[ne];
+    const int64_t mis = (int64_t)(((uintptr_t)codes & 15) / 2);
+    const int64_t a0 = c0 - ((c0 + mis) % 8);  // codes + a0 is 16-byte aligned
+    const int64_t nch = (c1 - a0 + 7) / 8;
+    const uint4 *src = reinterpret_cast<const uint4 *>(codes + a0);
+#pragma unroll 4
+    for (int64_t ch = threadIdx.x; ch < nch; ch += blockDim.x) {
+        const uint4 v = __ldg(src + ch);
+        const uint64_t lo = ((uint64_t)v.y << 32) | v.x, hi = ((uint64_t)v.w << 32) | v.z;
+        const uint64_t k1 = 0x0001000100010001ull, k8 = 0x8000800080008000ull;
+        if (!(((lo - k1) & ~lo & k8) | ((hi - k1) & ~hi & k8))) continue;  // no zero halfword
+        const uint16_t *cv = reinterpret_cast<const uint16_t *>(&v);
+        for (int t = 0; t < 8; t++) {
+            const int64_t q = a0 + ch * 8 + t;
+            if (cv[t] != 0 || q < c0 || q >= c1) continue;
+            int lo_e = 0, hi_e = ne - 1;  // largest e with s_base[e] <= q
+            while (lo_e < hi_e) {
+                const int mid = (lo_e + hi_e + 1) >> 1;
+                if (s_base[mid] <= q) lo_e = mid;
+                else hi_e = mid - 1;
+            }
+            atomicAdd(&s_cnt[lo_e], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) cnt[e0 + i] = s_cnt[i];
+}
+
 // Compress post-pass: outliers of every (item, warp) with escapes, in stream
 // order, read back from the grid (escaped points keep their originals).  One
 // warp screens 32 entries and replays only those that escaped.
@@ -2122,8 +2170,8 @@ static int sweep_run(hpez_plan plan, const void *orig, void *work, void *codes, 
         // outlier ranks: zero codes per (item, warp), then an exclusive scan
         const int64_t thr = ne * 32;
         if (p.d.code_dtype == HPEZ_CODES_U16)
-            count_zero_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>((const uint16_t *)codes, p.d_wbase, p.d_wn,
-                                                                             ne, p.d_esc_cnt);
+            count_zero_stream_kernel<<<(unsigned)((ne + kZeroEpb - 1) / kZeroEpb), 256, 0, st>>>(
+                (const uint16_t *)codes, p.d_wbase, p.d_wn, ne, p.d_esc_cnt);
         else
             count_zero_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>((const int32_t *)codes, p.d_wbase, p.d_wn,
                                                                              ne, p.d_esc_cnt);
