@@ -361,6 +361,28 @@ bool coarse_dsmem_build(const GridDev &g, const CommitDev *cms, const int *group
     const size_t smem = (size_t)D.P * D.L[1] * D.L[2] * (sizeof(double) + sizeof(uint16_t)) + 16 +
                         3 * kCoarseMaxCommits * sizeof(int32_t);
     if (smem > 200 * 1024) return false;
+    // the cluster must be schedulable here (non-portable sizes, MIG slices)
+    {
+        auto f = coarse_dsmem_kernel<HPEZ_COMPRESS>;
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1));
+        cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(ncta);
+        lc.blockDim = dim3(kCoarseDsmemThreads);
+        lc.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = ncta;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&nclusters, f, &lc) != cudaSuccess || nclusters < 1) {
+            cudaGetLastError();
+            return false;
+        }
+    }
     out->d = D;
     out->ncta = ncta;
     out->smem = smem;

@@ -2061,7 +2061,7 @@ int32_t hpez_plan_num_launches(hpez_plan plan) {
     if (!p.coarse_groups.empty()) n++;
     if (!p.flow_order.empty()) n++;
     n += (int)p.tiles.size();
-    n += 3;  // escape scan (3 kernels)
+    n += 1;  // escape scan (single-pass look-back kernel)
     n += 1;  // escape count pre-pass (decompress) or outlier gather (compress)
     if (p.d.with_stats && p.d.direction == HPEZ_COMPRESS) n += 2;
     return n;
