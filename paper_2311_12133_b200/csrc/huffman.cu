@@ -2,8 +2,9 @@
 // the drop-in for huffman.encode / decode (huffman.py:144-174) as used by
 // container.pack_codes / unpack_codes (container.py:70-106).
 //
-// * histogram: warp-aggregated (match_any) increments into a shared-memory
-//   window around the code centre, global atomics outside it.
+// * histogram: shared-memory window around the code centre (u16 streams:
+//   16-byte loads, privatized window copies; i32: warp-aggregated match_any),
+//   global atomics outside it.
 // * table: heap Huffman lengths with the (freq, smallest symbol) tie-break and
 //   canonical codes, on the host (<= 65,536 symbols).
 // * pack: chunks of 4096 codes; per-chunk bit counts -> scan -> each CTA
@@ -14,6 +15,7 @@
 //   table-driven decoder, both with the reference's error semantics.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <queue>
 #include <vector>
@@ -55,6 +57,50 @@ __global__ void __launch_bounds__(512) histogram_kernel(const C *__restrict__ co
     for (int i = threadIdx.x; i < kHistWindow; i += blockDim.x) {
         const uint32_t v = win[i];
         if (v && lo + i < nbins) atomicAdd(&counts[lo + i], v);
+    }
+}
+
+
+// u16 streams: eight codes per 16-byte load; each group of warps owns a
+// private copy of the shared-memory window (fewer same-address conflicts on
+// the concentrated centre bins), merged into the global counts at the end.
+constexpr int kHistCopies = 2;  // default window copies per CTA (HPEZ_HIST_COPIES)
+__global__ void __launch_bounds__(512) histogram_u16_kernel(const uint16_t *__restrict__ codes, int64_t n,
+                                                            uint32_t *__restrict__ counts, int64_t nbins,
+                                                            int64_t lo, int copies) {
+    extern __shared__ uint32_t hwin[];  // copies x kHistWindow
+    for (int i = threadIdx.x; i < copies * kHistWindow; i += blockDim.x) hwin[i] = 0;
+    __syncthreads();
+    uint32_t *win = hwin + ((threadIdx.x >> 5) % copies) * kHistWindow;
+    auto add = [&](uint32_t c) {
+        const int64_t w = (int64_t)c - lo;
+        if (w >= 0 && w < kHistWindow) atomicAdd(&win[w], 1u);
+        else if ((int64_t)c < nbins) atomicAdd(&counts[c], 1u);
+    };
+    // head up to 16-byte alignment, vector body, tail
+    const int64_t mis = (int64_t)(((uintptr_t)codes & 15) / 2);
+    const int64_t head = mis ? std::min<int64_t>(n, 8 - mis) : 0;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    if (gtid < head) add(codes[gtid]);
+    const int64_t nvec = (n - head) / 8;
+    const uint4 *v = reinterpret_cast<const uint4 *>(codes + head);
+#pragma unroll 2
+    for (int64_t k = gtid; k < nvec; k += nthr) {
+        const uint4 q = __ldg(v + k);
+        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            add(w4[j] & 0xffffu);
+            add(w4[j] >> 16);
+        }
+    }
+    for (int64_t i = head + nvec * 8 + gtid; i < n; i += nthr) add(codes[i]);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHistWindow; i += blockDim.x) {
+        uint32_t t = 0;
+        for (int c = 0; c < copies; c++) t += hwin[c * kHistWindow + i];
+        if (t && lo + i < nbins) atomicAdd(&counts[lo + i], t);
     }
 }
 
@@ -582,9 +628,16 @@ int hpez_histogram(const void *codes, int32_t code_dtype, int64_t n, uint32_t *c
     const int64_t centre = nbins / 2;
     const int64_t lo = std::max<int64_t>(0, centre - kHistWindow / 2);
     const int blocks = (int)std::min<int64_t>((n + 511) / 512, (int64_t)num_sms() * 4);
-    if (code_dtype == HPEZ_CODES_U16)
-        histogram_kernel<<<blocks, 512, 0, st>>>((const uint16_t *)codes, n, counts, nbins, lo);
-    else
+    if (code_dtype == HPEZ_CODES_U16) {
+        int copies = kHistCopies;
+        if (const char *ev = getenv("HPEZ_HIST_COPIES")) copies = std::max(1, std::min(6, atoi(ev)));
+        const size_t smem = sizeof(uint32_t) * copies * kHistWindow;
+        e = cudaFuncSetAttribute(histogram_u16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e) return cuda_ok(e);
+        const int per_sm = std::max(1, std::min(4, (int)(220 * 1024 / (smem + 1024))));
+        const int vb = (int)std::min<int64_t>((n / 8 + 511) / 512 + 1, (int64_t)num_sms() * per_sm);
+        histogram_u16_kernel<<<vb, 512, smem, st>>>((const uint16_t *)codes, n, counts, nbins, lo, copies);
+    } else
         histogram_kernel<<<blocks, 512, 0, st>>>((const int32_t *)codes, n, counts, nbins, lo);
     return cuda_ok(cudaGetLastError());
 }
