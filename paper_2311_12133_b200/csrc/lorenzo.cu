@@ -11,6 +11,7 @@
 // count / scan / rank pass, so the wavefront never needs an outlier cursor.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -90,6 +91,158 @@ __global__ void __launch_bounds__(128) lorenzo_plane_kernel(const LzGeom g, int6
         // _scan_decompress (lorenzo.py:117-128)
         work[i] = (T)round_native<ROUND>(__dadd_rn(acc, __dmul_rn(g.two_e, (double)(code - R))));
     }
+}
+
+
+// ---------------------------------------------------------- tile wavefront --
+// Rank <= 3 grids: 8^3 tiles on tile diagonals tz + ty + tx = D.  A tile
+// depends only on tiles of earlier diagonals (every stencil offset is
+// backward and <= 2 < 8), so one warp runs a tile through its 22 internal
+// hyperplanes lz + ly + lx = h (__syncwarp between them) and a grid barrier
+// separates diagonals: 128 global steps on cfg2 instead of 1024 launches.
+// Each warp stages its tile plus the 2-deep backward halo in shared memory.
+constexpr int kLzT = 8;
+constexpr int kLzH = 3 * (kLzT - 1) + 1;
+__constant__ uint16_t c_lt_pts[kLzT * kLzT * kLzT];  // (lz << 6) | (ly << 3) | lx, sorted by h
+__constant__ int16_t c_lt_off[kLzH + 1];
+
+constexpr int kLzS = kLzT + 2;  // staged tile edge: 2-deep backward halo
+constexpr int kLzTileThreads = 128;
+
+// One point of a staged tile: neighbours from the warp's shared-memory copy
+// sb (origin at tile - 2), reference term order, quantizer as in
+// lorenzo_plane_kernel; the result goes to sb and to the grid.
+template <typename T, typename C, int DIR, int ROUND>
+__device__ __forceinline__ void lz_tile_point(const LzGeom &g, double *sb, int lz, int ly, int lx, int64_t z, int64_t y,
+                                              int64_t x, T *__restrict__ work, C *__restrict__ codes, int64_t code) {
+    const int64_t c[4] = {0, z, y, x};
+    const int so = ((lz + 2) * kLzS + (ly + 2)) * kLzS + (lx + 2);
+    const int64_t i = z * g.estr[1] + y * g.estr[2] + x;
+    if (DIR == HPEZ_DECOMPRESS && code == 0) return;  // outlier already scattered (staged from work)
+    if (DIR == HPEZ_COMPRESS) code = 0;                // escape unless the quantizer accepts
+    double acc = 0.0;
+    for (int t = 0; t < c_lz.n; t++) {
+        bool ok = true;
+#pragma unroll
+        for (int a = 1; a < 4; a++) ok &= c[a] >= c_lz.delta[t][a];
+        if (ok) {
+            const int d = (c_lz.delta[t][1] * kLzS + c_lz.delta[t][2]) * kLzS + c_lz.delta[t][3];
+            acc = __dadd_rn(acc, __dmul_rn(c_lz.coef[t], sb[so - d]));
+        }
+    }
+    const int64_t R = g.radius;
+    if (DIR == HPEZ_COMPRESS) {
+        const double orig = sb[so];
+        if (g.bound > 0.0) {
+            const double q = __ddiv_rn(__dsub_rn(orig, acc), g.two_e);
+            double kq = floor(__dadd_rn(fabs(q), 0.5));
+            if (q < 0.0) kq = -kq;
+            if (-(double)R < kq && kq < (double)R) {
+                const double recon = round_native<ROUND>(__dadd_rn(acc, __dmul_rn(g.two_e, kq)));
+                if (fabs(__dsub_rn(recon, orig)) <= g.bound) {
+                    code = (int64_t)kq + R;
+                    sb[so] = recon;
+                    work[i] = (T)recon;
+                }
+            }
+        } else {
+            const double recon = round_native<ROUND>(acc);
+            if (recon == orig) {
+                code = R;
+                sb[so] = recon;
+                work[i] = (T)recon;
+            }
+        }
+        codes[i] = (C)code;
+    } else {
+        const double v = round_native<ROUND>(__dadd_rn(acc, __dmul_rn(g.two_e, (double)(code - R))));
+        sb[so] = v;
+        work[i] = (T)v;
+    }
+}
+
+template <typename T, typename C, int DIR, int ROUND>
+__global__ void __launch_bounds__(kLzTileThreads) lorenzo_tile_kernel(const LzGeom g, T *__restrict__ work,
+                                                                      C *__restrict__ codes, uint32_t *bar) {
+    __shared__ double s_tile[kLzTileThreads / 32][kLzS * kLzS * kLzS];  // one staged tile per warp (8 KB each)
+    __shared__ int32_t s_code[DIR == HPEZ_DECOMPRESS ? kLzTileThreads / 32 : 1][kLzT * kLzT * kLzT];
+    const int64_t Z = g.dims[1], Y = g.dims[2], X = g.dims[3];
+    const int ntz = (int)((Z + kLzT - 1) / kLzT), nty = (int)((Y + kLzT - 1) / kLzT), ntx = (int)((X + kLzT - 1) / kLzT);
+    const int ndiag = ntz + nty + ntx - 2;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double *sb = s_tile[wib];
+    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+    uint32_t target = 0;
+    for (int D = 0; D < ndiag; D++) {
+        const int tz0 = max(0, D - (nty - 1) - (ntx - 1)), tz1 = min(ntz - 1, D);
+        const int npair = (tz1 - tz0 + 1) * nty;
+        for (int k = gw; k < npair; k += nwarps) {
+            const int tz = tz0 + k / nty, ty = k % nty, tx = D - tz - ty;
+            if (tx < 0 || tx >= ntx) continue;
+            const int64_t z0 = (int64_t)tz * kLzT, y0 = (int64_t)ty * kLzT, x0 = (int64_t)tx * kLzT;
+            // stage the tile and its backward halo (earlier diagonals: final)
+            for (int q = lane; q < kLzS * kLzS * kLzS; q += 32) {
+                const int sz = q / (kLzS * kLzS), sy = (q / kLzS) % kLzS, sx = q % kLzS;
+                const int64_t z = z0 - 2 + sz, y = y0 - 2 + sy, x = x0 - 2 + sx;
+                double v = 0.0;
+                if (z >= 0 && y >= 0 && x >= 0 && z < Z && y < Y && x < X)
+                    v = (double)__ldcg(work + z * g.estr[1] + y * g.estr[2] + x);
+                sb[q] = v;
+            }
+            // decompress: the tile's codes, in h order
+            int32_t *sc = s_code[DIR == HPEZ_DECOMPRESS ? wib : 0];
+            if (DIR == HPEZ_DECOMPRESS)
+                for (int q = lane; q < kLzT * kLzT * kLzT; q += 32) {
+                    const int pk = c_lt_pts[q];
+                    const int64_t z = z0 + (pk >> 6), y = y0 + ((pk >> 3) & 7), x = x0 + (pk & 7);
+                    sc[q] = (z < Z && y < Y && x < X) ? (int32_t)__ldcg(codes + z * g.estr[1] + y * g.estr[2] + x) : 0;
+                }
+            __syncwarp();
+            for (int h = 0; h < kLzH; h++) {
+#pragma unroll 1
+                for (int q = c_lt_off[h] + lane; q < c_lt_off[h + 1]; q += 32) {
+                    const int pk = c_lt_pts[q];
+                    const int lz = pk >> 6, ly = (pk >> 3) & 7, lx = pk & 7;
+                    const int64_t z = z0 + lz, y = y0 + ly, x = x0 + lx;
+                    if (z < Z && y < Y && x < X)
+                        lz_tile_point<T, C, DIR, ROUND>(g, sb, lz, ly, lx, z, y, x, work, codes,
+                                                        DIR == HPEZ_DECOMPRESS ? (int64_t)sc[q] : 0);
+                }
+                __syncwarp();
+            }
+        }
+        // grid barrier between diagonals (all CTAs co-resident: cooperative launch)
+        __syncthreads();
+        target += gridDim.x;
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(bar, 1u);
+            while (ld_acquire(bar) < target) __nanosleep(32);
+        }
+        __syncthreads();
+    }
+}
+
+static bool lz_tile_table() {
+    static bool done = false;
+    if (done) return true;
+    uint16_t pts[kLzT * kLzT * kLzT];
+    int16_t off[kLzH + 1];
+    int k = 0;
+    for (int h = 0; h < kLzH; h++) {
+        off[h] = (int16_t)k;
+        for (int a = 0; a < kLzT; a++)
+            for (int b = 0; b < kLzT; b++) {
+                const int c = h - a - b;
+                if (c >= 0 && c < kLzT) pts[k++] = (uint16_t)((a << 6) | (b << 3) | c);
+            }
+    }
+    off[kLzH] = (int16_t)k;
+    if (cudaMemcpyToSymbol(c_lt_pts, pts, sizeof pts) != cudaSuccess) return false;
+    if (cudaMemcpyToSymbol(c_lt_off, off, sizeof off) != cudaSuccess) return false;
+    done = true;
+    return true;
 }
 
 template <typename C>
@@ -226,7 +379,42 @@ static int lorenzo_run(const LzGeom &g, int direction, int rounding, T *work, C 
         f = rounding == HPEZ_ROUND_F32 ? lorenzo_plane_kernel<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_F32>
           : rounding == HPEZ_ROUND_INT ? lorenzo_plane_kernel<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_INT>
                                        : lorenzo_plane_kernel<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_NONE>;
-    for (int64_t d = 0; d < planes; d++) f<<<grid, 128, 0, st>>>(g, d, work, codes);
+    // opt-in (HPEZ_LORENZO_TILE=1): bit-exact, but measured slower than the
+    // per-hyperplane launches on cfg2 so far (8.0 vs 7.2 ms, order 1)
+    const char *lt = getenv("HPEZ_LORENZO_TILE");
+    bool tiled = g.dims[0] == 1 && lt && atoi(lt) != 0 && lz_tile_table();
+    if (tiled) {
+        typedef void (*tf_t)(const LzGeom, T *, C *, uint32_t *);
+        tf_t tf;
+        if (direction == HPEZ_COMPRESS)
+            tf = rounding == HPEZ_ROUND_F32 ? lorenzo_tile_kernel<T, C, HPEZ_COMPRESS, HPEZ_ROUND_F32>
+               : rounding == HPEZ_ROUND_INT ? lorenzo_tile_kernel<T, C, HPEZ_COMPRESS, HPEZ_ROUND_INT>
+                                            : lorenzo_tile_kernel<T, C, HPEZ_COMPRESS, HPEZ_ROUND_NONE>;
+        else
+            tf = rounding == HPEZ_ROUND_F32 ? lorenzo_tile_kernel<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_F32>
+               : rounding == HPEZ_ROUND_INT ? lorenzo_tile_kernel<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_INT>
+                                            : lorenzo_tile_kernel<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_NONE>;
+        int occ = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tf, kLzTileThreads, 0) != cudaSuccess || occ < 1) occ = 1;
+        const int64_t pairs = ((g.dims[1] + kLzT - 1) / kLzT) * ((g.dims[2] + kLzT - 1) / kLzT);
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * sms, (pairs + 3) / 4));
+        uint32_t *bar = nullptr;
+        e = cudaMallocAsync((void **)&bar, sizeof(uint32_t), st);
+        if (!e) e = cudaMemsetAsync(bar, 0, sizeof(uint32_t), st);
+        if (e) return lz_cuda(e);
+        LzGeom gg = g;
+        void *args[] = {(void *)&gg, (void *)&work, (void *)&codes, (void *)&bar};
+        e = cudaLaunchCooperativeKernel((const void *)tf, dim3(blocks), dim3(kLzTileThreads), args, 0, st);
+        cudaFreeAsync(bar, st);
+        if (e) {
+            cudaGetLastError();
+            tiled = false;  // cooperative launch unavailable: hyperplane launches
+        }
+    }
+    if (!tiled)
+        for (int64_t d = 0; d < planes; d++) f<<<grid, 128, 0, st>>>(g, d, work, codes);
     if (direction == HPEZ_COMPRESS) compact(true);
     e = cudaGetLastError();
     uint64_t total = 0;

@@ -8,8 +8,15 @@ from golden import fixtures
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["hyperplanes", "tiles"])
+def lz_mode(request, monkeypatch):
+    # hyperplane launches (default) and the opt-in tile-wavefront kernel
+    monkeypatch.setenv("HPEZ_LORENZO_TILE", "1" if request.param == "tiles" else "0")
+    return request.param
+
+
 @pytest.mark.parametrize("fx", fixtures("lorenzo"), ids=lambda f: f.name)
-def test_lorenzo_matches_reference(fx):
+def test_lorenzo_matches_reference(fx, lz_mode):
     from paper_2311_12133_b200.lorenzo import lorenzo_pass
     m = fx.meta
     work = np.ascontiguousarray(fx["input"], dtype=np.float64)
@@ -24,7 +31,7 @@ def test_lorenzo_matches_reference(fx):
     assert fx.check("work_d", back)
 
 
-def test_lorenzo_large_vs_oracle():
+def test_lorenzo_large_vs_oracle(lz_mode):
     import synthetic as syn
     from oracle import oracle
     from paper_2311_12133_b200.lorenzo import lorenzo_pass
