@@ -331,7 +331,7 @@ def run_b200(args):
                      "frac": round(ach_c / peak, 4), "traffic": traffic,
                      "traffic_note": "ncu dram__bytes_read+write of one compress sweep "
                                      "(profiles/traffic_cfg2.json) over this run's sweep time, GB/s",
-                     "kernel": "compress sweep (coarse + flow + escape scan/gather kernels of one run_levels)",
+                     "kernel": "compress sweep (coarse DSMEM cluster + flow + escape scan/gather kernels of one run_levels)",
                      "algorithmic_bytes": f"{BYTES_COMPRESS} B/pt x {n} pts",
                      "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"},
         "e2e": {"value": round(world * gb / (e2e_ms / 1e3), 3), "unit": UNIT,

@@ -65,3 +65,37 @@ def test_coarse_cluster_sizes(monkeypatch):
     for n in ("1", "4", "8", "16"):
         monkeypatch.setenv("HPEZ_COARSE_CLUSTER", n)
         _roundtrip(data, levels, md)
+
+
+@pytest.mark.parametrize("shift", [1, 3, 6])
+def test_misaligned_code_buffers(shift):
+    # the escape gather, the zero-count pre-pass and the histogram read codes
+    # with aligned 16-byte loads around arbitrary element offsets
+    import torch
+
+    from oracle import oracle
+    from paper_2311_12133_b200 import huffman
+    from paper_2311_12133_b200.interp import codes_to_int32, run_levels_device
+    rng = np.random.default_rng(shift)
+    dims = (45, 52, 61)
+    data = (_field(50 + shift, dims) + rng.standard_normal(dims).astype(np.float32) * 0.2).astype(np.float32)
+    e = 1e-6 * float(data.max() - data.min())
+    levels = _levels(50 + shift, 64, e, 4, 1)
+    md = np.array([0.3, 0.3, 0.4])
+    lv = [_Spec(t) for t in levels]
+    ref = data.astype(np.float64)
+    c_o, o_o = oracle.run_levels(ref, levels, direction="compress", radius=32768, md_alpha=md, rounding=1)
+    assert o_o.size > 100
+    big = torch.zeros(c_o.size + 16, dtype=torch.uint16, device="cuda")
+    view = big[shift:shift + c_o.size]
+    work = torch.from_numpy(data).cuda()
+    codes, outl, n_out = run_levels_device(work, lv, direction="compress", radius=32768, md_alpha=md,
+                                           rounding=1, codes=view)
+    assert np.array_equal(codes_to_int32(codes), c_o)
+    assert outl[:n_out].cpu().numpy().tobytes() == o_o.tobytes()
+    assert np.array_equal(huffman.histogram_device(view), np.bincount(c_o))
+    back = torch.zeros_like(work)
+    back[::64, ::64, ::64] = work[::64, ::64, ::64]
+    run_levels_device(back, lv, direction="decompress", radius=32768, md_alpha=md, rounding=1,
+                      codes=view, outliers=outl[:n_out])
+    assert torch.equal(back, work)
