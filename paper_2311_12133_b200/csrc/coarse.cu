@@ -82,7 +82,7 @@ __device__ __forceinline__ void coarse_point(const CoarseDesc &D, const CoarseCt
             if (a == 0) {
                 int zz = z + u;
                 zz = zz < 0 ? 0 : (zz >= X.L0 ? X.L0 - 1 : zz);  // clamped rows are never used
-                const uint32_t owner = (uint32_t)(zz / X.P);
+                const uint32_t owner = fdiv((uint32_t)zz, D.fd_P);
                 const uint32_t la = X.sbase + (uint32_t)((((zz - (int)owner * X.P) * X.L1 + y) * X.L2 + x) * 8);
                 v[t][i] = ld_dsmem(la, owner);
             } else if (a == 1) {
@@ -358,6 +358,7 @@ bool coarse_dsmem_build(const GridDev &g, const CommitDev *cms, const int *group
     ncta = (D.L[0] + D.P - 1) / D.P;
     D.fd_plane = make_fastdiv((uint32_t)(D.L[1] * D.L[2]));
     D.fd_x = make_fastdiv((uint32_t)D.L[2]);
+    D.fd_P = make_fastdiv((uint32_t)D.P);
     const size_t smem = (size_t)D.P * D.L[1] * D.L[2] * (sizeof(double) + sizeof(uint16_t)) + 16 +
                         3 * kCoarseMaxCommits * sizeof(int32_t);
     if (smem > 200 * 1024) return false;

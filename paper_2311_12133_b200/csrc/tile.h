@@ -108,7 +108,7 @@ struct CoarseDesc {
     int64_t n_codes;
     int32_t grp_off[kCoarseMaxGroups + 1];
     int32_t lvl_s[kCoarseMaxLevels], lvl_sh[kCoarseMaxLevels];
-    FastDiv fd_plane, fd_x;         // division by L1*L2 and by L2
+    FastDiv fd_plane, fd_x, fd_P;   // division by L1*L2, by L2 and by P
     int8_t lut[kCoarseMaxLevels][64];
     CoarseCommit c[kCoarseMaxCommits];
 };
