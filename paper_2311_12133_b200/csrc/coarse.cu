@@ -42,14 +42,19 @@ template <int KIND> __device__ constexpr int ck_axis(int t) {
     return KIND < 3 ? KIND : KIND == 3 ? (t == 0 ? 0 : 1) : KIND == 4 ? (t == 0 ? 0 : 2) : KIND == 5 ? (t == 0 ? 1 : 2) : t;
 }
 
-// Outlier of the zero code at position pos of commit cm (see tile.cu)
-__device__ __noinline__ double coarse_outlier(const CoarseCommit &cm, const TileRun &A, int64_t pos) {
-    const int64_t item = pos / cm.p_item;
-    const int64_t w = (pos - item * cm.p_item) / cm.pw;
-    const int64_t e = (int64_t)(cm.item_base + item) * kItemWarps + w;
-    const uint16_t *codes = (const uint16_t *)A.codes + cm.code_base;
-    int64_t r = A.esc_off[e];
-    for (int64_t q = item * cm.p_item + w * cm.pw; q < pos; q++) r += codes[q] == 0;
+// Outlier of the zero code at position pos of commit cm.  The coarse levels
+// are the stream prefix [0, n_cc), so the rank is the number of zero codes
+// before the point's stream index: a per-CTA prefix over 256-code chunks
+// (zpre) plus a scan inside the chunk.  Independent of the decompress
+// pre-pass, which therefore runs concurrently on a side stream.
+constexpr int kCoarseZChunk = 256;
+__device__ __noinline__ double coarse_outlier(const CoarseCommit &cm, const TileRun &A, int64_t pos,
+                                              const uint32_t *zpre) {
+    const int64_t q = cm.code_base + pos;
+    const uint16_t *codes = (const uint16_t *)A.codes;
+    const int64_t c = q / kCoarseZChunk;
+    int64_t r = zpre[c];
+    for (int64_t k = c * kCoarseZChunk; k < q; k++) r += codes[k] == 0;
     if (r < A.outl_cap) return A.outl[r];
     atomicExch(A.flags, HPEZ_OUTLIER_UNDERFLOW);
     return 0.0;
@@ -64,7 +69,7 @@ struct CoarseCtx {
 template <int DIR, int KIND, int FAM>
 __device__ __forceinline__ void coarse_point(const CoarseDesc &D, const CoarseCtx &X, const TileRun &A, double *slab,
                                              uint16_t *ccode, const CoarseCommit &cm, int z, int y, int x, int li,
-                                             int64_t pos) {
+                                             int64_t pos, const uint32_t *zpre) {
     constexpr int NAX = KIND < 3 ? 1 : KIND < 6 ? 2 : 3;
     constexpr int NF = Fam<FAM>::n;
     const int s = cm.s;
@@ -123,7 +128,7 @@ __device__ __forceinline__ void coarse_point(const CoarseDesc &D, const CoarseCt
     } else {
         const int64_t code = (int64_t)__double_as_longlong(slab[li]);
         const double val = code != 0 ? dequantize_point<HPEZ_ROUND_F32>(pred, code, cm.two_e, (int64_t)R)
-                                     : (double)(float)coarse_outlier(cm, A, pos);
+                                     : (double)(float)coarse_outlier(cm, A, pos, zpre);
         slab[li] = val;
     }
     (void)gidx;
@@ -132,10 +137,10 @@ __device__ __forceinline__ void coarse_point(const CoarseDesc &D, const CoarseCt
 template <int DIR>
 __device__ __forceinline__ void coarse_dispatch(const CoarseDesc &D, const CoarseCtx &X, const TileRun &A, double *slab,
                                                 uint16_t *ccode, const CoarseCommit &cm, int z, int y, int x, int li,
-                                                int64_t pos) {
+                                                int64_t pos, const uint32_t *zpre) {
 #define HPEZ_CK(K, F)                                                      \
     case K * 5 + F:                                                        \
-        coarse_point<DIR, K, F>(D, X, A, slab, ccode, cm, z, y, x, li, pos); \
+        coarse_point<DIR, K, F>(D, X, A, slab, ccode, cm, z, y, x, li, pos, zpre); \
         return;
     switch (cm.kind * 5 + cm.fam) {
         HPEZ_CK(0, 0) HPEZ_CK(0, 1) HPEZ_CK(0, 2) HPEZ_CK(0, 3) HPEZ_CK(0, 4)
@@ -188,6 +193,18 @@ __global__ void __launch_bounds__(kCoarseDsmemThreads, 1) coarse_dsmem_kernel(co
     int32_t *c_iz0 = reinterpret_cast<int32_t *>((reinterpret_cast<uintptr_t>(ccode + (size_t)D.P * plane) + 15) &
                                                  ~(uintptr_t)15);
     int32_t *c_n = c_iz0 + kCoarseMaxCommits, *c_pre = c_n + kCoarseMaxCommits;
+    uint32_t *c_zpre = reinterpret_cast<uint32_t *>(c_pre + kCoarseMaxCommits);  // decompress: zero-code prefix per chunk
+    const int nzc = (D.n_cc + kCoarseZChunk - 1) / kCoarseZChunk;
+    if (DIR == HPEZ_DECOMPRESS) {
+        const int wq = threadIdx.x >> 5, ln = threadIdx.x & 31;
+        for (int c = wq; c < nzc; c += (int)(blockDim.x >> 5)) {
+            uint32_t z = 0;
+            for (int k = c * kCoarseZChunk + ln; k < min((c + 1) * kCoarseZChunk, D.n_cc); k += 32)
+                z += ((const uint16_t *)A.codes)[k] == 0;
+            for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+            if (ln == 0) c_zpre[c + 1] = z;
+        }
+    }
     if ((int)threadIdx.x < D.n_commits) {
         const CoarseCommit &cm = D.c[threadIdx.x];
         const int iz0 = X.z0 <= cm.st[0] ? 0 : (X.z0 - cm.st[0] + cm.sp[0] - 1) >> cm.sh[0];
@@ -196,6 +213,10 @@ __global__ void __launch_bounds__(kCoarseDsmemThreads, 1) coarse_dsmem_kernel(co
         c_n[threadIdx.x] = max(0, iz1 - iz0 + 1) * cm.cnt[1] * cm.cnt[2];
     }
     __syncthreads();
+    if (DIR == HPEZ_DECOMPRESS && threadIdx.x == blockDim.x - 1) {  // exclusive prefix (runs beside the group prefix)
+        c_zpre[0] = 0;
+        for (int c = 1; c <= nzc; c++) c_zpre[c] += c_zpre[c - 1];
+    }
     if (threadIdx.x < D.n_groups) {
         int acc = 0;
         for (int c = D.grp_off[threadIdx.x]; c < D.grp_off[threadIdx.x + 1]; c++) {
@@ -237,7 +258,7 @@ __global__ void __launch_bounds__(kCoarseDsmemThreads, 1) coarse_dsmem_kernel(co
             const int z = cm.st[0] + (iz << cm.sh[0]), y = cm.st[1] + (iy << cm.sh[1]), x = cm.st[2] + (ix << cm.sh[2]);
             const int li = ((z - X.z0) * X.L1 + y) * X.L2 + x;
             const int64_t pos = ((int64_t)iz * cm.cnt[1] + iy) * cm.cnt[2] + ix;
-            coarse_dispatch<DIR>(D, X, A, slab, ccode, cm, z, y, x, li, pos);
+            coarse_dispatch<DIR>(D, X, A, slab, ccode, cm, z, y, x, li, pos, c_zpre);
         }
         cl_sync();
     }
@@ -359,8 +380,14 @@ bool coarse_dsmem_build(const GridDev &g, const CommitDev *cms, const int *group
     D.fd_plane = make_fastdiv((uint32_t)(D.L[1] * D.L[2]));
     D.fd_x = make_fastdiv((uint32_t)D.L[2]);
     D.fd_P = make_fastdiv((uint32_t)D.P);
+    int64_t ncc = 0;
+    for (int k = 0; k < n; k++) ncc = std::max<int64_t>(ncc, D.c[k].code_base + (int64_t)D.c[k].cnt[0] * D.c[k].cnt[1] * D.c[k].cnt[2]);
+    for (int k = 0; k < n; k++) if (D.c[k].code_base < 0) return false;
+    if (ncc >= (1ll << 30)) return false;
+    D.n_cc = (int32_t)ncc;
     const size_t smem = (size_t)D.P * D.L[1] * D.L[2] * (sizeof(double) + sizeof(uint16_t)) + 16 +
-                        3 * kCoarseMaxCommits * sizeof(int32_t);
+                        3 * kCoarseMaxCommits * sizeof(int32_t) +
+                        (size_t)((ncc + kCoarseZChunk - 1) / kCoarseZChunk + 1) * sizeof(uint32_t);
     if (smem > 200 * 1024) return false;
     // the cluster must be schedulable here (non-portable sizes, MIG slices)
     {

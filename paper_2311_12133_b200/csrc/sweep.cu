@@ -1257,6 +1257,8 @@ struct Plan {
     std::vector<int> coarse_group;  // (level, depth) group of each coarse commit
     CoarsePlan cplan;               // coarse levels in distributed shared memory (coarse.cu)
     bool coarse_dsmem = false;
+    cudaStream_t side = nullptr;    // decompress: the zero-count pre-pass runs beside the coarse kernel
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
     // device
     CommitDev *d_commits = nullptr;
@@ -1290,6 +1292,9 @@ struct Plan {
                         d_mixed_items, d_cbase, d_cn, d_clevel, d_errbuf, d_csum, d_orig_scratch};
         for (void *p : ptrs)
             if (p) cudaFree(p);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (side) cudaStreamDestroy(side);
     }
 
     std::vector<std::vector<int>> order_candidates() const {  // plan.py:37-51
@@ -2166,16 +2171,37 @@ static int sweep_run(hpez_plan plan, const void *orig, void *work, void *codes, 
     A.errbuf = p.d_errbuf;
     A.dense = stat_dense;
     const KernelSet ks = pick(p.d);
+    // decompress with the DSMEM coarse kernel: it ranks its own outliers (the
+    // coarse levels are the stream prefix), so the zero-count pre-pass only
+    // has to finish before the flow kernel and runs on a side stream
+    const bool fork = p.d.direction == HPEZ_DECOMPRESS && p.coarse_dsmem && !getenv("HPEZ_NO_FORK");
+    cudaStream_t pst = st;
+    if (fork) {
+        if (!p.side) {
+            e = cudaStreamCreateWithFlags(&p.side, cudaStreamNonBlocking);
+            if (!e) e = cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming);
+            if (!e) e = cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming);
+            if (e) return cuda_status(e);
+        }
+        e = cudaEventRecord(p.ev_fork, st);
+        if (!e) e = cudaStreamWaitEvent(p.side, p.ev_fork, 0);
+        if (e) return cuda_status(e);
+        pst = p.side;
+    }
     if (p.d.direction == HPEZ_DECOMPRESS) {
         // outlier ranks: zero codes per (item, warp), then an exclusive scan
         const int64_t thr = ne * 32;
         if (p.d.code_dtype == HPEZ_CODES_U16)
-            count_zero_stream_kernel<<<(unsigned)((ne + kZeroEpb - 1) / kZeroEpb), 256, 0, st>>>(
+            count_zero_stream_kernel<<<(unsigned)((ne + kZeroEpb - 1) / kZeroEpb), 256, 0, pst>>>(
                 (const uint16_t *)codes, p.d_wbase, p.d_wn, ne, p.d_esc_cnt);
         else
-            count_zero_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>((const int32_t *)codes, p.d_wbase, p.d_wn,
-                                                                             ne, p.d_esc_cnt);
-        exclusive_scan(p.d_esc_cnt, ne, p.d_esc_off, p.d_scan_tmp, p.d_total, st);
+            count_zero_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, pst>>>((const int32_t *)codes, p.d_wbase, p.d_wn,
+                                                                              ne, p.d_esc_cnt);
+        exclusive_scan(p.d_esc_cnt, ne, p.d_esc_off, p.d_scan_tmp, p.d_total, pst);
+    }
+    if (fork) {
+        e = cudaEventRecord(p.ev_join, p.side);
+        if (e) return cuda_status(e);
     }
     if (p.coarse_dsmem) {
         if (p.d.direction == HPEZ_COMPRESS && p.c_coarse < (int)p.commits.size()) {
@@ -2188,6 +2214,7 @@ static int sweep_run(hpez_plan plan, const void *orig, void *work, void *codes, 
         }
         TileRun cr{orig, work, codes, outliers, A.outl_cap, p.d_esc_cnt, p.d_esc_off, p.d_counters + 1};
         e = coarse_dsmem_launch(p.cplan, p.d.direction, cr, st);
+        if (!e && fork) e = cudaStreamWaitEvent(st, p.ev_join, 0);
         if (e) return cuda_status(e);
     } else if (!p.coarse_groups.empty()) {
         sweep_fn f = (p.coarse_fast && ks.coarse_fast) ? ks.coarse_fast : ks.coarse;

@@ -106,6 +106,7 @@ struct CoarseDesc {
     int32_t R;
     int32_t n_commits, n_groups, n_levels;
     int64_t n_codes;
+    int32_t n_cc;                  // codes of the coarse levels = stream prefix [0, n_cc)
     int32_t grp_off[kCoarseMaxGroups + 1];
     int32_t lvl_s[kCoarseMaxLevels], lvl_sh[kCoarseMaxLevels];
     FastDiv fd_plane, fd_x, fd_P;   // division by L1*L2, by L2 and by P
