@@ -62,22 +62,30 @@ static __global__ void __launch_bounds__(kScanBlock) scan_single_kernel(const V 
         s_w[lane] = w;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
+        // warp-wide look-back: lane j inspects tile (lb - 1 - j); the
+        // closest predecessor with an inclusive prefix ends the walk
         const int64_t agg = s_w[31];
+        if (tile > 0 && lane == 0) scan_st_release(status + tile, kScanFlagA | (unsigned long long)agg);
         int64_t excl = 0;
-        if (tile > 0) {
-            scan_st_release(status + tile, kScanFlagA | (unsigned long long)agg);
-            for (int64_t j = tile - 1;; j--) {
-                unsigned long long sv;
+        for (int64_t lb = tile; lb > 0; lb -= 32) {
+            const int64_t j = lb - 1 - lane;
+            unsigned long long sv = 0;
+            if (j >= 0)
                 while (((sv = scan_ld_acquire(status + j)) >> 62) == 0) {
                 }
-                excl += (int64_t)(sv & kScanVal);
-                if ((sv & ~kScanVal) == kScanFlagP) break;
-            }
+            const uint32_t pm = __ballot_sync(0xffffffffu, j >= 0 && (sv & ~kScanVal) == kScanFlagP);
+            const int stop = pm ? __ffs(pm) - 1 : 32;  // first lane (closest tile) holding a prefix
+            int64_t pv = (j >= 0 && lane <= stop) ? (int64_t)(sv & kScanVal) : 0;
+            for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+            excl += pv;
+            if (pm) break;
         }
-        scan_st_release(status + tile, kScanFlagP | (unsigned long long)(excl + agg));
-        s_prefix = excl;
-        if (tile == tiles - 1 && total) *total = excl + agg;
+        if (lane == 0) {
+            scan_st_release(status + tile, kScanFlagP | (unsigned long long)(excl + agg));
+            s_prefix = excl;
+            if (tile == tiles - 1 && total) *total = excl + agg;
+        }
     }
     __syncthreads();
     int64_t run = s_prefix + (warp ? s_w[warp - 1] : 0) + x - t;
