@@ -89,7 +89,7 @@ struct GridDev {
     int32_t dims[kMaxRank];
     int32_t estr[kMaxRank];     // element strides
     int32_t bstr[kMaxRank];     // block-grid strides (row-major block index)
-    int32_t pad;
+    int32_t bs_log2;            // log2(block_size) when it is a power of two, else -1
     int64_t npts;
     int64_t nblk;               // blocks per table level
     int64_t radius;
@@ -119,8 +119,9 @@ struct CommitDev {
     int32_t tag_off;            // mixed: TagInfo slot 0 of the class
     int32_t slot_off;           // mixed: 256-entry tag->slot map
     int32_t commit_id;
-    int32_t fast_id;            // rank-3 uniform specialisation, -1 = generic path
-    PredDev pred;               // uniform commits
+    int32_t fast_id;            // rank-3 uniform specialisation; -2 = mixed fast path; -1 = generic
+    PredDev pred;               // uniform commits; mixed: the class's MD blend weights
+    uint8_t tdesc[64];          // mixed fast path: tag -> (split axis + 1) << 6 | fast_id
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {

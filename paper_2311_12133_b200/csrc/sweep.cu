@@ -704,6 +704,177 @@ __device__ __forceinline__ void process_dispatch(const SweepArgs &A, const Commi
 #undef HPEZ_FAST
 }
 
+// ------------------------------------------- mixed commits, fast path --
+// One point's prediction for a rank-3 layout KIND and family FAM: every
+// stencil value is loaded with an in-grid (clamped) address in one round
+// trip; edge lanes take the truncated row (kernels.resolve_row).
+template <typename T, int KIND, int FAM>
+__device__ __forceinline__ double pred_point(const T *__restrict__ work, int idx, const int (&crd)[3],
+                                             const int (&Dv)[3], const int (&sEv)[3], int s, double w0, double w1,
+                                             double w2) {
+    constexpr int NAX = KIND < 3 ? 1 : KIND < 6 ? 2 : 3;
+    T v[NAX][6];
+#pragma unroll
+    for (int t = 0; t < NAX; t++) {
+        const int a = kind_axis<KIND>(t);
+#pragma unroll
+        for (int i = 0; i < Fam<FAM>::n; i++) {
+            const int u = Fam<FAM>::u(i);
+            const int cc = crd[a] + u * s;
+            const bool ok = u < 0 ? cc >= 0 : cc <= Dv[a] - 1;
+            v[t][i] = work[ok ? idx + u * sEv[a] : idx];
+        }
+    }
+    double pt[NAX];
+#pragma unroll
+    for (int t = 0; t < NAX; t++) {
+        const int a = kind_axis<KIND>(t);
+        if (Fam<FAM>::interior(crd[a], Dv[a], s)) {
+            pt[t] = Fam<FAM>::combine(v[t]);
+        } else {
+            double xv[6];
+#pragma unroll
+            for (int i = 0; i < 6; i++) xv[i] = i < Fam<FAM>::n ? (double)v[t][i] : 0.0;
+            pt[t] = edge_row<FAM>(xv, crd[a], Dv[a], s);
+        }
+    }
+    if (NAX == 1) return pt[0];
+    if (NAX == 2) return DA(DM(w0, pt[0]), DM(w1, pt[NAX - 1]));
+    return DA(DA(DM(w0, pt[0]), DM(w1, pt[1])), DM(w2, pt[NAX - 1]));
+}
+
+template <typename T>
+__device__ __noinline__ double mixed_pred(int fid, const T *__restrict__ work, int idx, const int (&crd)[3],
+                                          const int (&Dv)[3], const int (&sEv)[3], int s, double w0, double w1,
+                                          double w2) {
+#define HPEZ_MP(K, F) \
+    case K * 5 + F:   \
+        return pred_point<T, K, F>(work, idx, crd, Dv, sEv, s, w0, w1, w2);
+    switch (fid) {
+        HPEZ_MP(0, 0) HPEZ_MP(0, 1) HPEZ_MP(0, 2) HPEZ_MP(0, 3) HPEZ_MP(0, 4)
+        HPEZ_MP(1, 0) HPEZ_MP(1, 1) HPEZ_MP(1, 2) HPEZ_MP(1, 3) HPEZ_MP(1, 4)
+        HPEZ_MP(2, 0) HPEZ_MP(2, 1) HPEZ_MP(2, 2) HPEZ_MP(2, 3) HPEZ_MP(2, 4)
+        HPEZ_MP(3, 0) HPEZ_MP(3, 1) HPEZ_MP(3, 2)
+        HPEZ_MP(4, 0) HPEZ_MP(4, 1) HPEZ_MP(4, 2)
+        HPEZ_MP(5, 0) HPEZ_MP(5, 1) HPEZ_MP(5, 2)
+        HPEZ_MP(6, 0) HPEZ_MP(6, 1) HPEZ_MP(6, 2)
+    default:
+        return 0.0;  // unreachable: the planner only emits the ids above
+    }
+#undef HPEZ_MP
+}
+
+// Mixed commit (interp.py:350-411) of a rank-3 grid: per point, the block
+// tag (power-of-two block size: shifts) selects a precomputed descriptor
+// held with the commit in shared memory -- membership rule (split axis)
+// and specialised predictor -- so the dependent chain before the stencil
+// loads is one table byte.  Lanes of one warp that disagree on the
+// predictor take their switch cases one after the other.
+template <typename T, typename C, int DIR, int ROUND>
+__device__ __forceinline__ void process_mixed(const SweepArgs &A, const CommitDev &cm, int item, int warp) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t p0 = (uint32_t)(item - cm.item_base) * (uint32_t)cm.p_item + (uint32_t)warp * (uint32_t)cm.pw;
+    const uint32_t pend = min(p0 + (uint32_t)cm.pw, cm.npos);
+    const int e = item * kItemWarps + warp;
+    if (p0 >= pend) {
+        if (DIR == HPEZ_COMPRESS && lane == 0) A.esc_cnt[e] = 0;
+        return;
+    }
+    const int st0 = cm.start[0], st1 = cm.start[1], st2 = cm.start[2];
+    const int sp0 = cm.step[0], sp1 = cm.step[1], sp2 = cm.step[2];
+    const int cn1 = cm.cnt[1], cn2 = cm.cnt[2];
+    const int Dv[3] = {A.g.dims[0], A.g.dims[1], A.g.dims[2]};
+    const int E0 = A.g.estr[0], E1 = A.g.estr[1];
+    const int s = cm.s;
+    const int sEv[3] = {s * E0, s * E1, s};
+    const double bound = cm.bound, two_e = cm.two_e, inv_two_e = cm.inv_two_e;
+    const double w0 = cm.pred.w[0], w1 = cm.pred.w[1], w2 = cm.pred.w[2];
+    const int64_t R = A.g.radius;
+    const int32_t R32 = (int32_t)R;
+    const double Rd = (double)R;
+    const bool isA = cm.kind == COMMIT_MIXED_A;
+    const uint32_t present = cm.axes_present;
+    const int phase = cm.phase;
+    const int bsh = A.g.bs_log2, bs0 = A.g.bstr[0], bs1 = A.g.bstr[1];
+    const uint8_t *__restrict__ tl = A.table + (int64_t)cm.level * A.g.nblk;
+    T *__restrict__ work = (T *)A.work;
+    const T *__restrict__ origp = (const T *)A.orig;
+    const bool oop = A.orig != A.work;
+    C *__restrict__ codes = (C *)A.codes;
+    int64_t cbase = A.wbase[e];
+    const int64_t obase = DIR == HPEZ_DECOMPRESS ? A.esc_off[e] : 0;
+    uint32_t nesc = 0;
+    uint32_t p = p0 + lane;
+    uint32_t r = fdiv(p, cm.fd[2]);
+    int jx = (int)(p - r * (uint32_t)cn2);
+    uint32_t q = fdiv(r, cm.fd[1]);
+    int jy = (int)(r - q * (uint32_t)cn1);
+    int jz = (int)q;
+    for (uint32_t pb = p0; pb < pend; pb += 32) {
+        const bool valid = pb + lane < pend;
+        const int crd[3] = {st0 + jz * sp0, st1 + jy * sp1, st2 + jx * sp2};
+        const int idx = crd[0] * E0 + crd[1] * E1 + crd[2];
+        bool member = false;
+        int fid = 0;
+        if (valid) {
+            const int tag = __ldg(tl + (crd[0] >> bsh) * bs0 + (crd[1] >> bsh) * bs1 + (crd[2] >> bsh));
+            const int desc = cm.tdesc[tag & 63];
+            const int sp = (desc >> 6) - 1;
+            const uint32_t jodd = (uint32_t)(jz & 1) | (uint32_t)(jy & 1) << 1 | (uint32_t)(jx & 1) << 2;
+            if (isA) member = sp < 0 || !((jodd >> sp) & 1u);
+            else member = sp >= 0 && ((jodd >> sp) & 1u) && __popc(present & jodd & ~(1u << sp)) == phase;
+            fid = desc & 63;
+        }
+        const uint32_t mb = __ballot_sync(0xffffffffu, member);
+        const int64_t ci = cbase + __popc(mb & ((1u << lane) - 1u));
+        bool esc = false;
+        if (member) {
+            if (DIR == HPEZ_COMPRESS) {
+                const T o = origp[idx];
+                const double pred = mixed_pred<T>(fid, work, idx, crd, Dv, sEv, s, w0, w1, w2);
+                double out;
+                const int32_t c = quantize_point<ROUND>((double)o, pred, bound, two_e, inv_two_e, Rd, R32, &out);
+                codes[ci] = (C)c;
+                esc = c == 0;
+                if (!esc || oop) work[idx] = (T)out;
+            } else {
+                const int64_t code = (int64_t)codes[ci];
+                if (code != 0) {
+                    const double pred = mixed_pred<T>(fid, work, idx, crd, Dv, sEv, s, w0, w1, w2);
+                    work[idx] = (T)dequantize_point<ROUND>(pred, code, two_e, R);
+                } else {
+                    esc = true;
+                }
+            }
+        }
+        const uint32_t eb = __ballot_sync(0xffffffffu, esc);
+        if (DIR == HPEZ_DECOMPRESS && esc) {
+            const int64_t o = obase + nesc + __popc(eb & ((1u << lane) - 1u));
+            if (o < A.outl_cap) __stcg(work + idx, (T)A.outl[o]);
+            else atomicExch(A.flags, HPEZ_OUTLIER_UNDERFLOW);
+        }
+        nesc += __popc(eb);
+        cbase += __popc(mb);
+        jx += 32;
+        while (jx >= cn2) {
+            jx -= cn2;
+            if (++jy >= cn1) {
+                jy = 0;
+                jz++;
+            }
+        }
+    }
+    if (DIR == HPEZ_COMPRESS && lane == 0) A.esc_cnt[e] = nesc;
+}
+
+// Fast kernels: uniform commits through their specialisation, mixed
+// commits through process_mixed.
+template <typename T, typename C, int DIR, int ROUND>
+__device__ __forceinline__ void process_any_fast(const SweepArgs &A, const CommitDev &cm, int item, int warp) {
+    if (cm.fast_id >= 0) process_dispatch<T, C, DIR, ROUND>(A, cm, item, warp);
+    else process_mixed<T, C, DIR, ROUND>(A, cm, item, warp);
+}
+
 // Leading small levels on one thread-block cluster (up to 16 CTAs x 1024
 // threads, one per SM).  Every coarse commit descriptor sits in shared
 // memory; the commits of one (level, DAG depth) group are independent, so
@@ -735,7 +906,7 @@ __global__ void __launch_bounds__(kCoarseThreads, 1) coarse_kernel(const __grid_
         for (int u = gw; u < (t1 - t0) * kItemWarps; u += nwarps) {
             const int t = t0 + u / kItemWarps;
             const int c = A.coarse_pairs[2 * t], item = A.coarse_pairs[2 * t + 1];
-            if (FAST) process_dispatch<T, C, DIR, ROUND>(A, s_cm[c], item, u % kItemWarps);
+            if (FAST) process_any_fast<T, C, DIR, ROUND>(A, s_cm[c], item, u % kItemWarps);
             else process_warp<T, C, DIR, ROUND, STATS>(A, s_cm[c], item, u % kItemWarps);
         }
         cluster_sync_all();
@@ -836,7 +1007,7 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? HPEZ_FLOW_OCC * 8 / kItem
         }
         __syncthreads();  // B
         const long long c2 = A.prof ? clock64() : 0;
-        if (FAST) process_dispatch<T, C, DIR, ROUND>(A, s_cm, item, warp);
+        if (FAST) process_any_fast<T, C, DIR, ROUND>(A, s_cm, item, warp);
         else process_warp<T, C, DIR, ROUND, STATS>(A, s_cm, item, warp);
         if (threadIdx.x == 0) {  // nobody reads s_item / s_next again before barrier A
             s_item = q_cur;
@@ -1462,6 +1633,9 @@ struct Plan {
             }
             nblk_table = nb;
             g.nblk = nb;
+            g.bs_log2 = -1;
+            for (int k = 0; k < 31; k++)
+                if ((int64_t)1 << k == d.block_size) g.bs_log2 = k;
             table.assign(d.block_table, d.block_table + (size_t)nb * d.n_levels);
         }
         int64_t code_pos = 0;
@@ -1579,6 +1753,26 @@ struct Plan {
             slots[slot_off + t] = (uint8_t)slot++;
         }
         const int nph = __builtin_popcount(axes_present);
+        // mixed fast path: tag -> (split + 1) << 6 | specialisation of the
+        // commit-A (inter-level) and commit-B (same-level) predictors
+        bool mfast = true;
+        uint8_t desc_a[64] = {}, desc_b[64] = {};
+        for (int t : present) {
+            const TagInfo &ti = tags[tag_off + slots[slot_off + t]];
+            const int fa = fast_id_pred(ti.inter);
+            const int fb = ti.split >= 0 ? fast_id_pred(ti.same) : 0;
+            if (t >= 64 || fa < 0 || fb < 0) {
+                mfast = false;
+                continue;
+            }
+            desc_a[t] = (uint8_t)(((ti.split + 1) << 6) | fa);
+            desc_b[t] = (uint8_t)(((ti.split + 1) << 6) | fb);
+        }
+        Cfg mdc;
+        mdc.md = 1;
+        mdc.spline = 0;
+        mdc.same = 0;
+        const PredDev mdw = make_pred(mdc, v, false);  // MD blend weights depend on the class only
         for (int ph = -1; ph < nph; ph++) {
             CommitDev cm = base_commit(li, start, step, count);
             cm.kind = ph < 0 ? COMMIT_MIXED_A : COMMIT_MIXED_B;
@@ -1587,6 +1781,9 @@ struct Plan {
             cm.tag_off = tag_off;
             cm.slot_off = slot_off;
             cm.code_base = -1;
+            cm.pred = mdw;
+            memcpy(cm.tdesc, ph < 0 ? desc_a : desc_b, 64);
+            cm.fast_id = mfast ? -2 : -1;
             commits.push_back(cm);
             uint32_t vm = 0;
             for (int a : v) vm |= 1u << a;
@@ -1597,10 +1794,9 @@ struct Plan {
         return 0;
     }
 
-    // Rank-3 uniform specialisation id (KIND * 5 + FAM) or -1.
-    int fast_id_of(const CommitDev &cm) const {
-        if (d.rank != 3 || cm.kind != COMMIT_UNIFORM || d.with_stats) return -1;
-        const PredDev &p = cm.pred;
+    // Rank-3 specialisation id (KIND * 5 + FAM) of one predictor, or -1.
+    int fast_id_pred(const PredDev &p) const {
+        if (d.rank != 3) return -1;
         if (!p.md) return p.axis * 5 + p.fam;
         if (p.fam > FAM_NAT_I) return -1;
         if (p.nax == 3) return 6 * 5 + p.fam;
@@ -1608,6 +1804,15 @@ struct Plan {
         const int a = p.axes[0], b = p.axes[1];
         const int kind = (a == 0 && b == 1) ? 3 : (a == 0 && b == 2) ? 4 : (a == 1 && b == 2) ? 5 : -1;
         return kind < 0 ? -1 : kind * 5 + p.fam;
+    }
+
+    // Uniform commits: their specialisation id or -1.  Mixed commits: -2
+    // (process_mixed) when every tag has a specialisation, the grid is
+    // rank 3 and the block size a power of two; else -1 (generic path).
+    int fast_id_of(const CommitDev &cm) const {
+        if (d.rank != 3 || d.with_stats) return -1;
+        if (cm.kind != COMMIT_UNIFORM) return (cm.fast_id == -2 && g.bs_log2 >= 0) ? -2 : -1;
+        return fast_id_pred(cm.pred);
     }
 
     // Item interval of commit `pv` covering the outer-axis window of item
@@ -1813,7 +2018,7 @@ struct Plan {
             CommitDev &cm = commits[ci];
             cm.fast_id = fast_id_of(cm);
             bool &f = ci < c_coarse ? coarse_fast : flow_fast;
-            f = f && cm.fast_id >= 0;
+            f = f && cm.fast_id != -1;
         }
         if (getenv("HPEZ_COARSE_GENERIC")) coarse_fast = false;
     }

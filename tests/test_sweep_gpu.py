@@ -85,7 +85,8 @@ def _random_case(seed, dims, anchor=64, bs=16, table=True, rounding=0, e=1e-3):
 
 @pytest.mark.parametrize("seed,dims,bs,rounding", [
     (1, (70, 66, 90), 16, 1), (2, (65, 130, 33), 32, 0), (3, (129, 100, 57), 8, 1),
-    (4, (300, 257), 16, 1), (5, (40, 30, 20, 24), 8, 0)])
+    (4, (300, 257), 16, 1), (5, (40, 30, 20, 24), 8, 0), (6, (70, 66, 90), 24, 1),
+    (7, (97, 64, 130), 32, 0)])
 def test_sweep_random_tables_vs_oracle(seed, dims, bs, rounding):
     from paper_2311_12133_b200.interp import CodeSource, run_levels
     data, levels, tbl, md = _random_case(seed, dims, bs=bs, rounding=rounding)
