@@ -170,6 +170,12 @@ int hpez_plan_level_codes(hpez_plan plan, int64_t *out);
  * memory (coarse.cu). */
 int hpez_plan_info(hpez_plan plan, int64_t *out);
 
+/* Diagnostics: per commit, 6 values [kind (0 uniform, 1 mixed A, 2 mixed B),
+ * level, lattice positions, items, members, fast id]; members are read from
+ * the device tables, so the plan must have run once.  Returns the number of
+ * commits written (at most cap / 6) or a negative status. */
+int32_t hpez_plan_commit_stats(hpez_plan plan, int64_t *out, int32_t cap);
+
 /* HPEZ_PROFILE plans only: out[0..24) per-level (first item start, last
  * item end) globaltimer stamps of the flow kernel, 12 levels x 2; out[24..72)
  * per-level accumulated (grab, wait, work) SM cycles and item count, 12 x 4. */

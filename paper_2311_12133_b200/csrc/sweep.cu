@@ -708,11 +708,17 @@ __device__ __forceinline__ void process_dispatch(const SweepArgs &A, const Commi
 // One point's prediction for a rank-3 layout KIND and family FAM: every
 // stencil value is loaded with an in-grid (clamped) address in one round
 // trip; edge lanes take the truncated row (kernels.resolve_row).
+struct Pt3 {  // one point of a rank-3 grid: coordinates, extents, element steps of stride s
+    int crd[3], Dv[3], sEv[3];
+};
+
 template <typename T, int KIND, int FAM>
-__device__ __forceinline__ double pred_point(const T *__restrict__ work, int idx, const int (&crd)[3],
-                                             const int (&Dv)[3], const int (&sEv)[3], int s, double w0, double w1,
-                                             double w2) {
+__device__ __forceinline__ double pred_point(const T *__restrict__ work, int idx, const Pt3 &P, int s, double w0,
+                                             double w1, double w2) {
     constexpr int NAX = KIND < 3 ? 1 : KIND < 6 ? 2 : 3;
+    const int(&crd)[3] = P.crd;
+    const int(&Dv)[3] = P.Dv;
+    const int(&sEv)[3] = P.sEv;
     T v[NAX][6];
 #pragma unroll
     for (int t = 0; t < NAX; t++) {
@@ -744,12 +750,11 @@ __device__ __forceinline__ double pred_point(const T *__restrict__ work, int idx
 }
 
 template <typename T>
-__device__ __noinline__ double mixed_pred(int fid, const T *__restrict__ work, int idx, const int (&crd)[3],
-                                          const int (&Dv)[3], const int (&sEv)[3], int s, double w0, double w1,
-                                          double w2) {
+__device__ __forceinline__ double mixed_pred(int fid, const T *__restrict__ work, int idx, const Pt3 &P, int s,
+                                             double w0, double w1, double w2) {
 #define HPEZ_MP(K, F) \
     case K * 5 + F:   \
-        return pred_point<T, K, F>(work, idx, crd, Dv, sEv, s, w0, w1, w2);
+        return pred_point<T, K, F>(work, idx, P, s, w0, w1, w2);
     switch (fid) {
         HPEZ_MP(0, 0) HPEZ_MP(0, 1) HPEZ_MP(0, 2) HPEZ_MP(0, 3) HPEZ_MP(0, 4)
         HPEZ_MP(1, 0) HPEZ_MP(1, 1) HPEZ_MP(1, 2) HPEZ_MP(1, 3) HPEZ_MP(1, 4)
@@ -783,10 +788,15 @@ __device__ __forceinline__ void process_mixed(const SweepArgs &A, const CommitDe
     const int st0 = cm.start[0], st1 = cm.start[1], st2 = cm.start[2];
     const int sp0 = cm.step[0], sp1 = cm.step[1], sp2 = cm.step[2];
     const int cn1 = cm.cnt[1], cn2 = cm.cnt[2];
-    const int Dv[3] = {A.g.dims[0], A.g.dims[1], A.g.dims[2]};
     const int E0 = A.g.estr[0], E1 = A.g.estr[1];
     const int s = cm.s;
-    const int sEv[3] = {s * E0, s * E1, s};
+    Pt3 P;
+    P.Dv[0] = A.g.dims[0];
+    P.Dv[1] = A.g.dims[1];
+    P.Dv[2] = A.g.dims[2];
+    P.sEv[0] = s * E0;
+    P.sEv[1] = s * E1;
+    P.sEv[2] = s;
     const double bound = cm.bound, two_e = cm.two_e, inv_two_e = cm.inv_two_e;
     const double w0 = cm.pred.w[0], w1 = cm.pred.w[1], w2 = cm.pred.w[2];
     const int64_t R = A.g.radius;
@@ -802,6 +812,10 @@ __device__ __forceinline__ void process_mixed(const SweepArgs &A, const CommitDe
     const bool oop = A.orig != A.work;
     C *__restrict__ codes = (C *)A.codes;
     int64_t cbase = A.wbase[e];
+    if (A.wn[e] == 0) {  // no member in this warp's range (typical of B commits)
+        if (DIR == HPEZ_COMPRESS && lane == 0) A.esc_cnt[e] = 0;
+        return;
+    }
     const int64_t obase = DIR == HPEZ_DECOMPRESS ? A.esc_off[e] : 0;
     uint32_t nesc = 0;
     uint32_t p = p0 + lane;
@@ -810,17 +824,33 @@ __device__ __forceinline__ void process_mixed(const SweepArgs &A, const CommitDe
     uint32_t q = fdiv(r, cm.fd[1]);
     int jy = (int)(r - q * (uint32_t)cn1);
     int jz = (int)q;
+    auto tag_at = [&](int x, int y, int z, bool ok) {
+        return ok ? (int)__ldg(tl + (z >> bsh) * bs0 + (y >> bsh) * bs1 + (x >> bsh)) : 0;
+    };
+    // the next iteration's tag is loaded one iteration ahead
+    int tag_next = tag_at(st2 + jx * sp2, st1 + jy * sp1, st0 + jz * sp0, p0 + lane < pend);
     for (uint32_t pb = p0; pb < pend; pb += 32) {
         const bool valid = pb + lane < pend;
-        const int crd[3] = {st0 + jz * sp0, st1 + jy * sp1, st2 + jx * sp2};
-        const int idx = crd[0] * E0 + crd[1] * E1 + crd[2];
+        P.crd[0] = st0 + jz * sp0;
+        P.crd[1] = st1 + jy * sp1;
+        P.crd[2] = st2 + jx * sp2;
+        const int idx = P.crd[0] * E0 + P.crd[1] * E1 + P.crd[2];
+        const int tag = tag_next;
+        const uint32_t jodd = (uint32_t)(jz & 1) | (uint32_t)(jy & 1) << 1 | (uint32_t)(jx & 1) << 2;
+        jx += 32;
+        while (jx >= cn2) {
+            jx -= cn2;
+            if (++jy >= cn1) {
+                jy = 0;
+                jz++;
+            }
+        }
+        tag_next = tag_at(st2 + jx * sp2, st1 + jy * sp1, st0 + jz * sp0, pb + 32 + lane < pend);
         bool member = false;
         int fid = 0;
         if (valid) {
-            const int tag = __ldg(tl + (crd[0] >> bsh) * bs0 + (crd[1] >> bsh) * bs1 + (crd[2] >> bsh));
             const int desc = cm.tdesc[tag & 63];
             const int sp = (desc >> 6) - 1;
-            const uint32_t jodd = (uint32_t)(jz & 1) | (uint32_t)(jy & 1) << 1 | (uint32_t)(jx & 1) << 2;
             if (isA) member = sp < 0 || !((jodd >> sp) & 1u);
             else member = sp >= 0 && ((jodd >> sp) & 1u) && __popc(present & jodd & ~(1u << sp)) == phase;
             fid = desc & 63;
@@ -831,7 +861,7 @@ __device__ __forceinline__ void process_mixed(const SweepArgs &A, const CommitDe
         if (member) {
             if (DIR == HPEZ_COMPRESS) {
                 const T o = origp[idx];
-                const double pred = mixed_pred<T>(fid, work, idx, crd, Dv, sEv, s, w0, w1, w2);
+                const double pred = mixed_pred<T>(fid, work, idx, P, s, w0, w1, w2);
                 double out;
                 const int32_t c = quantize_point<ROUND>((double)o, pred, bound, two_e, inv_two_e, Rd, R32, &out);
                 codes[ci] = (C)c;
@@ -840,7 +870,7 @@ __device__ __forceinline__ void process_mixed(const SweepArgs &A, const CommitDe
             } else {
                 const int64_t code = (int64_t)codes[ci];
                 if (code != 0) {
-                    const double pred = mixed_pred<T>(fid, work, idx, crd, Dv, sEv, s, w0, w1, w2);
+                    const double pred = mixed_pred<T>(fid, work, idx, P, s, w0, w1, w2);
                     work[idx] = (T)dequantize_point<ROUND>(pred, code, two_e, R);
                 } else {
                     esc = true;
@@ -855,14 +885,6 @@ __device__ __forceinline__ void process_mixed(const SweepArgs &A, const CommitDe
         }
         nesc += __popc(eb);
         cbase += __popc(mb);
-        jx += 32;
-        while (jx >= cn2) {
-            jx -= cn2;
-            if (++jy >= cn1) {
-                jy = 0;
-                jz++;
-            }
-        }
     }
     if (DIR == HPEZ_COMPRESS && lane == 0) A.esc_cnt[e] = nesc;
 }
@@ -2308,6 +2330,25 @@ int hpez_plan_info(hpez_plan plan, int64_t *out) {
             for (int i = 0; i < 4; i++) out[8 + i] = (int64_t)h[i];
     }
     return HPEZ_OK;
+}
+
+int32_t hpez_plan_commit_stats(hpez_plan plan, int64_t *out, int32_t cap) {
+    if (!plan || !out || cap < 6) return -HPEZ_BAD_ARGUMENT;
+    const Plan &p = plan->p;
+    if (!p.setup_done) return -HPEZ_BAD_ARGUMENT;
+    std::vector<int32_t> wn((size_t)std::max(p.n_items, 1) * kItemWarps);
+    if (cudaMemcpy(wn.data(), p.d_wn, wn.size() * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -HPEZ_CUDA_ERROR;
+    int32_t k = 0;
+    for (size_t c = 0; c < p.commits.size() && (k + 1) * 6 <= cap; c++, k++) {
+        const CommitDev &cm = p.commits[c];
+        int64_t m = 0;
+        for (int64_t e = (int64_t)cm.item_base * kItemWarps; e < (int64_t)(cm.item_base + cm.n_items) * kItemWarps; e++)
+            m += wn[e];
+        const int64_t v[6] = {cm.kind, cm.level, cm.npos, cm.n_items, m, cm.fast_id};
+        for (int i = 0; i < 6; i++) out[6 * k + i] = v[i];
+    }
+    return k;
 }
 
 int hpez_plan_level_codes(hpez_plan plan, int64_t *out) {

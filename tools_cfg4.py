@@ -28,7 +28,11 @@ ap.add_argument("--eps", type=float, default=1e-3)
 ap.add_argument("--dims", default=None)
 ap.add_argument("--no-oracle", action="store_true")
 ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--uniform", action="store_true", help="drop the block table (uniform commits)")
+ap.add_argument("--profile", action="store_true", help="per-level flow-kernel timeline (HPEZ_PROFILE)")
 args = ap.parse_args()
+if args.profile:
+    os.environ["HPEZ_PROFILE"] = "1"
 dev = torch.device("cuda", 0)
 torch.cuda.set_device(0)
 dims = tuple(int(x) for x in args.dims.split(",")) if args.dims else None
@@ -64,6 +68,9 @@ if cfg.block_table is not None:
 if cfg.predictor == "interp":
     from paper_2311_12133_b200.container import parse_config, serialize_config
     cfg = parse_config(serialize_config(cfg, g.dims), g.dims)
+    if args.uniform:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, block_size=0, block_table=None)
     levels = _plan(g.dims, cfg).levels
     frozen = () if cfg.frozen_dim is None else (cfg.frozen_dim,)
     kw = dict(radius=cfg.radius, frozen_axes=frozen, md_alpha=np.asarray(cfg.md_alpha), rounding=1,
@@ -82,6 +89,18 @@ if cfg.predictor == "interp":
     out["num_launches"] = pc.num_launches
     codes = torch.empty(pc.num_codes, dtype=torch.uint16, device=dev)
     outl = torch.empty(pc.num_codes, dtype=torch.float64, device=dev)
+    if args.profile:  # one cold compress, then the timeline (counters accumulate across runs)
+        w.copy_(orig)
+        run_levels_device(w, levels, direction="compress", codes=codes, outliers=outl, **kw)
+        tl = np.zeros(72, dtype=np.int64)
+        _lib.lib().hpez_plan_levels_timeline(pc.handle, tl.ctypes.data)
+        t0 = min(x for x in tl[0:24:2] if 0 < x < 2**62)
+        out["level_us"] = [(l, round((tl[2*l]-t0)/1e3, 1), round((tl[2*l+1]-t0)/1e3, 1)) for l in range(12) if tl[2*l+1] > 0]
+        cs = np.zeros(6 * 4096, dtype=np.int64)
+        ncm = _lib.lib().hpez_plan_commit_stats(pc.handle, cs.ctypes.data, cs.size)
+        out["commits"] = cs[:6 * max(ncm, 0)].reshape(-1, 6).tolist()  # kind, level, npos, items, members, fast id
+        out["level_cycles_per_item"] = {l: [int(x / max(tl[27 + 4*l], 1)) for x in tl[24 + 4*l: 27 + 4*l]] + [int(tl[27 + 4*l])]
+                                        for l in range(12) if tl[27 + 4*l]}
     tc, td = [], []
     for it in range(args.iters + 2):
         w.copy_(orig)
