@@ -5,6 +5,8 @@ edge stencils would change, so the archive would no longer match the
 reference).  Field i belongs to rank i % world_size.  Every rank compresses
 its own fields with the full B200 pipeline, then
 
+Peers are addressed by group rank (``group_peer``), so subgroups work.
+
 * all ranks learn every archive's size with one all-reduce of an int64
   vector (``ncclAllReduce`` over NVLink on GPUs, gloo on CPU), and
 * rank 0 receives the archives with batched point-to-point transfers
@@ -52,11 +54,11 @@ def gather_archives(local: dict, n_fields: int, group=None) -> list | None:
                 continue
             buf = torch.empty(sizes_h[i], dtype=torch.uint8, device=dev)
             recv[i] = buf
-            ops.append(dist.P2POp(dist.irecv, buf, src, group=group))
+            ops.append(dist.P2POp(dist.irecv, buf, group=group, group_peer=src))
     else:
         for i in sorted(local):
             t = torch.frombuffer(bytearray(local[i]), dtype=torch.uint8).to(dev)
-            ops.append(dist.P2POp(dist.isend, t, 0, group=group))
+            ops.append(dist.P2POp(dist.isend, t, group=group, group_peer=0))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
@@ -76,7 +78,7 @@ def scatter_archives(archives: Sequence[bytes] | None, n_fields: int, group=None
     if rank == 0:
         for i, a in enumerate(archives):
             sizes[i] = len(a)
-    dist.broadcast(sizes, 0, group=group)
+    dist.broadcast(sizes, group=group, group_src=0)
     sizes_h = sizes.cpu().tolist()
     mine, ops, recv = {}, [], {}
     for i in range(n_fields):
@@ -86,11 +88,11 @@ def scatter_archives(archives: Sequence[bytes] | None, n_fields: int, group=None
                 mine[i] = archives[i]
             else:
                 t = torch.frombuffer(bytearray(archives[i]), dtype=torch.uint8).to(dev)
-                ops.append(dist.P2POp(dist.isend, t, dst, group=group))
+                ops.append(dist.P2POp(dist.isend, t, group=group, group_peer=dst))
         elif dst == rank:
             buf = torch.empty(sizes_h[i], dtype=torch.uint8, device=dev)
             recv[i] = buf
-            ops.append(dist.P2POp(dist.irecv, buf, 0, group=group))
+            ops.append(dist.P2POp(dist.irecv, buf, group=group, group_peer=0))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
@@ -105,15 +107,16 @@ def compress_fields(make_field: Callable[[int], object], n_fields: int, bound, *
 
     ``make_field(i)`` builds (or loads) field i on its owner only.  ``codec``
     defaults to the B200 ``pipeline.compress`` (returning ``.archive``)."""
-    if codec is None:
-        from .pipeline import compress
-
-        def codec(grid, spec, **k):
-            return compress(grid, spec, **k).archive
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    mine = [i for i in range(n_fields) if owner(i, world) == rank]
     local = {}
-    for i in range(n_fields):
-        if owner(i, world) == rank:
+    if codec is None:
+        # B200 pipeline: field i's host zlib stage overlaps field i+1's GPU stage
+        from .pipeline import compress_many
+        for i, res in zip(mine, compress_many((make_field(i) for i in mine), bound, **kw)):
+            local[i] = res.archive
+    else:
+        for i in mine:
             local[i] = codec(make_field(i), bound, **kw)
     return gather_archives(local, n_fields, group=group)
 

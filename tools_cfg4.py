@@ -102,6 +102,7 @@ if cfg.predictor == "interp":
         out["level_cycles_per_item"] = {l: [int(x / max(tl[27 + 4*l], 1)) for x in tl[24 + 4*l: 27 + 4*l]] + [int(tl[27 + 4*l])]
                                         for l in range(12) if tl[27 + 4*l]}
     tc, td = [], []
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" isolates the sweeps
     for it in range(args.iters + 2):
         w.copy_(orig)
         flush.fill_(1.0)
@@ -118,6 +119,7 @@ if cfg.predictor == "interp":
         if it >= 2:
             tc.append(e[0].elapsed_time(e[1]))
             td.append(e[2].elapsed_time(e[3]))
+    torch.cuda.nvtx.range_pop()
     _, _, n_out = run_levels_device(w.copy_(orig), levels, direction="compress", codes=codes,
                                     outliers=outl, **kw)
     back.copy_(a0)

@@ -2,7 +2,7 @@
 tools_sweep_time.py into profiles/traffic_cfg2.json: per-kernel time and DRAM
 traffic of the last compress and the last decompress sweep.
 
-usage: python tools_traffic.py <ncu csv> <out json> <source note>
+usage: python tools_traffic.py <ncu csv> <out json> <source note> [points] [round]
 """
 import csv, json, sys
 
@@ -48,8 +48,8 @@ def main():
     c, d = groups(ks)
     summ = lambda g: [{"kernel": k["kernel"][:70], "us": round(k["us"], 3),
                        "dram_MB": round(k.get("dram_bytes", 0) / 1e6, 3)} for k in g]
-    n = 256 * 384 * 384
-    out = {"round": 1, "source": sys.argv[3],
+    n = int(sys.argv[4]) if len(sys.argv) > 4 else 256 * 384 * 384
+    out = {"round": int(sys.argv[5]) if len(sys.argv) > 5 else 1, "source": sys.argv[3],
            "compress_sweep_kernels": summ(c),
            "compress_sweep_us": round(sum(k["us"] for k in c), 3),
            "compress_dram_bytes_per_sweep": sum(k.get("dram_bytes", 0) for k in c),
