@@ -73,10 +73,16 @@ typedef struct {
 typedef struct hpez_plan_s *hpez_plan;
 
 /* Build the commit schedule of run_levels for one geometry/config
- * (interp.py:415-433 class enumeration, :322-411 commit split).  The plan
- * owns its device metadata and scratch; one run at a time per plan. */
+ * (interp.py:415-433 class enumeration, :322-411 commit split).  Host-side
+ * only (no device allocation).  One run at a time per plan. */
 int hpez_plan_create(const hpez_sweep_desc *desc, hpez_plan *out);
 int hpez_plan_destroy(hpez_plan plan);
+/* Device workspace of a plan (its commit / item tables and run scratch):
+ * the caller allocates `bytes` of device memory and binds it once, before
+ * the first run; runs then never allocate.  A plan run without a bound
+ * workspace makes one allocation of this size itself at its first run. */
+int hpez_plan_workspace_size(hpez_plan plan, int64_t *bytes);
+int hpez_plan_bind_workspace(hpez_plan plan, void *workspace, int64_t bytes);
 /* Number of codes the sweep produces / consumes (= points - anchors). */
 int64_t hpez_plan_num_codes(hpez_plan plan);
 int32_t hpez_plan_num_commits(hpez_plan plan);
@@ -87,7 +93,8 @@ int32_t hpez_plan_num_launches(hpez_plan plan);
  * outliers (f64, stream order).  Decompress: reads `codes_avail` codes and
  * `outl_cap` outliers; fewer codes than the plan needs -> CORRUPT_STREAM.
  * Stats (compress, with_stats plans): stat_err_sum/stat_count (device,
- * n_levels) are accumulated like PassStats.record; stat_dense (device,
+ * n_levels) are accumulated like PassStats.record (both may be null when
+ * only the dense grids are wanted: tune_blocks); stat_dense (device,
  * n_levels * points doubles, zero-initialised) receives the dense error
  * grids.  Launches are asynchronous on `stream`; call hpez_sweep_finish. */
 int hpez_sweep_run(hpez_plan plan, void *work, void *codes, int64_t codes_avail,

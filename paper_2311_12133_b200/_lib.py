@@ -62,6 +62,8 @@ def lib():
         "hpez_plan_num_launches": (I32, [P]),
         "hpez_plan_level_codes": (I32, [P, P]),
         "hpez_plan_info": (I32, [P, P]),
+        "hpez_plan_workspace_size": (I32, [P, P]),
+        "hpez_plan_bind_workspace": (I32, [P, P, I64]),
         "hpez_plan_commit_stats": (I32, [P, P, I32]),
         "hpez_plan_levels_timeline": (I32, [P, P]),
         "hpez_sweep_run": (I32, [P, P, P, I64, P, I64, P, P, P, P]),

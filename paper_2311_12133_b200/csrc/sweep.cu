@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "pairwise.cuh"
 #include "scan.cuh"
 #include "stencil.cuh"
 #include "tile.h"
@@ -1268,68 +1269,20 @@ __global__ void __launch_bounds__(256) mixed_count_kernel(const __grid_constant_
 }
 
 // ---------------------------------------------------- stats (tuning) --
-__device__ double leaf_sum(const double *a, int64_t n) {
-    if (n < 8) {
-        double r = -0.0;
-        for (int64_t i = 0; i < n; i++) r = __dadd_rn(r, a[i]);
-        return r;
-    }
-    double r[8];
-    for (int j = 0; j < 8; j++) r[j] = a[j];
-    int64_t i;
-    for (i = 8; i < n - (n % 8); i += 8)
-        for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; i++) res = __dadd_rn(res, a[i]);
-    return res;
-}
-
-// numpy pairwise sum of each commit's member errors (numpy order).
-__global__ void commit_pairwise_kernel(const double *errbuf, const int64_t *commit_code_base,
-                                       const int64_t *commit_n, double *commit_sum) {
+// numpy pairwise sum of each commit's member errors (numpy order), one CTA
+// of 256 threads per commit (pairwise.cuh).
+__global__ void __launch_bounds__(256) commit_pairwise_kernel(const double *errbuf, const int64_t *commit_code_base,
+                                                              const int64_t *commit_n, double *commit_sum) {
+    __shared__ double s_val[256];
+    __shared__ int8_t s_leaf[256];
     const int c = blockIdx.x;
     const int64_t base = commit_code_base[c], n = commit_n[c];
-    if (threadIdx.x != 0) return;
     if (n == 0) {
-        commit_sum[c] = 0.0;
+        if (threadIdx.x == 0) commit_sum[c] = 0.0;
         return;
     }
-    double vs[64];
-    int64_t fs[64], fn[64];
-    int32_t state[64];
-    int vt = 0, top = 1;
-    fs[0] = 0;
-    fn[0] = n;
-    state[0] = 0;
-    while (top) {
-        const int t = top - 1;
-        if (fn[t] <= 128) {
-            vs[vt++] = leaf_sum(errbuf + base + fs[t], fn[t]);
-            top--;
-            continue;
-        }
-        int64_t n2 = fn[t] / 2;
-        n2 -= n2 % 8;
-        if (state[t] == 0) {
-            state[t] = 1;
-            fs[top] = fs[t];
-            fn[top] = n2;
-            state[top] = 0;
-            top++;
-        } else if (state[t] == 1) {
-            state[t] = 2;
-            fs[top] = fs[t] + n2;
-            fn[top] = fn[t] - n2;
-            state[top] = 0;
-            top++;
-        } else {
-            const double b = vs[--vt], a = vs[--vt];
-            vs[vt++] = __dadd_rn(a, b);
-            top--;
-        }
-    }
-    commit_sum[c] = vs[0];
+    const double r = np_pairwise_cta<8>(errbuf + base, n, s_val, s_leaf);
+    if (threadIdx.x == 0) commit_sum[c] = r;
 }
 
 __global__ void stats_accumulate_kernel(int n_commits, const int32_t *commit_level, const double *commit_sum,
@@ -1474,17 +1427,18 @@ struct Plan {
     int32_t *d_clevel = nullptr;
     double *d_errbuf = nullptr, *d_csum = nullptr;
     unsigned long long *d_prof = nullptr;
+    std::vector<int32_t> clevel;    // level of each commit (stats accumulation)
+    bool profile = false;           // HPEZ_PROFILE at plan creation
     bool setup_done = false;
     int64_t outl_cap_last = 0;
     int flow_grid = 0;
 
+    void *ws = nullptr;             // device workspace (caller-bound or own_ws)
+    size_t ws_bytes = 0;
+    void *own_ws = nullptr;         // allocated by the plan only when no workspace was bound
+
     ~Plan() {
-        void *ptrs[] = {d_prof, d_commits, d_item_commit, d_flow_order, d_dep_off, d_coarse_pairs, d_coarse_groups,
-                        d_dep_rng, d_wbase, d_wn, d_esc_cnt, d_esc_off,
-                        d_scan_tmp, d_total, d_done, d_counters, d_tags, d_slots, d_table,
-                        d_mixed_items, d_cbase, d_cn, d_clevel, d_errbuf, d_csum, d_orig_scratch};
-        for (void *p : ptrs)
-            if (p) cudaFree(p);
+        if (own_ws) cudaFree(own_ws);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
         if (side) cudaStreamDestroy(side);
@@ -2089,17 +2043,67 @@ struct Plan {
     }
 };
 
-template <typename T>
-static cudaError_t dalloc(T **p, size_t n) {
-    if (n == 0) n = 1;
-    return cudaMalloc((void **)p, n * sizeof(T));
+// Device workspace layout: every table and scratch array of a plan carved
+// from one caller-provided block (hpez_plan_workspace_size / _bind), so a
+// run never allocates.  Offsets are 256-byte aligned.
+struct Carver {
+    char *base;
+    size_t off = 0;
+    template <typename T>
+    void take(T **p, size_t n) {
+        off = (off + 255) & ~(size_t)255;
+        *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+        off += std::max<size_t>(n, 1) * sizeof(T);
+    }
+};
+
+static bool plan_stats(const Plan &p) { return p.d.with_stats && p.d.direction == HPEZ_COMPRESS; }
+
+static size_t plan_layout(Plan &p, char *base) {
+    Carver c{base};
+    const size_t ni = (size_t)std::max(p.n_items, 1);
+    const size_t ne = ni * kItemWarps;
+    const size_t ntiles = (ne + kScanTile - 1) / kScanTile + 1;
+    const size_t nc = std::max<size_t>(p.commits.size(), 1);
+    c.take(&p.d_commits, p.commits.size());
+    c.take(&p.d_item_commit, p.item_commit.size());
+    c.take(&p.d_flow_order, p.flow_order.size());
+    c.take(&p.d_dep_off, p.dep_off.size());
+    c.take(&p.d_dep_rng, p.dep_rng.size());
+    c.take(&p.d_coarse_pairs, p.coarse_pairs.size());
+    c.take(&p.d_coarse_groups, p.coarse_groups.size());
+    c.take(&p.d_wn, p.wn.size());
+    c.take(&p.d_wbase, ne);
+    c.take(&p.d_esc_cnt, ne);
+    c.take(&p.d_esc_off, ne);
+    c.take(&p.d_scan_tmp, ntiles);
+    c.take(&p.d_total, 4);
+    c.take(&p.d_done, ni);
+    c.take(&p.d_counters, 4);
+    c.take(&p.d_tags, p.tags.size());
+    c.take(&p.d_slots, p.slots.size());
+    c.take(&p.d_table, p.table.size());
+    c.take(&p.d_mixed_items, p.mixed_items.size());
+    c.take(&p.d_clevel, nc);
+    c.take(&p.d_cbase, nc);
+    c.take(&p.d_cn, nc);
+    if (plan_stats(p)) {
+        c.take(&p.d_csum, nc);
+        c.take(&p.d_errbuf, (size_t)std::max<int64_t>(p.num_codes, 1));
+    }
+    if (p.profile) c.take(&p.d_prof, 96);
+    if (!p.tiles.empty() && p.d.direction == HPEZ_COMPRESS) {
+        char *o;
+        c.take(&o, (size_t)p.g.npts * (p.d.work_dtype == HPEZ_WORK_F32 ? 4 : 8));
+        p.d_orig_scratch = o;
+    }
+    return c.off + 256;
 }
 
 template <typename T>
-static cudaError_t dupload(T **p, const std::vector<T> &v) {
-    cudaError_t e = dalloc(p, v.size());
-    if (e == cudaSuccess && !v.empty()) e = cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
-    return e;
+static cudaError_t up(T *d, const std::vector<T> &v, cudaStream_t st) {
+    if (v.empty()) return cudaSuccess;
+    return cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st);
 }
 
 static int cuda_status(cudaError_t e) {
@@ -2190,41 +2194,32 @@ static SweepArgs base_args(Plan &p) {
 
 static int plan_setup(Plan *p, cudaStream_t st) {
     cudaError_t e = cudaSuccess;
-    const size_t ni = (size_t)std::max(p->n_items, 1);
-    const size_t ne = ni * kItemWarps;
-    const size_t ntiles = (ne + kScanTile - 1) / kScanTile + 1;
-    e = dupload(&p->d_commits, p->commits);
-    if (!e) e = dupload(&p->d_item_commit, p->item_commit);
-    if (!e) e = dupload(&p->d_flow_order, p->flow_order);
-    if (!e) e = dupload(&p->d_dep_off, p->dep_off);
-    if (!e) e = dupload(&p->d_dep_rng, p->dep_rng);
-    if (!e) e = dupload(&p->d_coarse_pairs, p->coarse_pairs);
-    if (!e) e = dupload(&p->d_coarse_groups, p->coarse_groups);
-    if (!e) e = dupload(&p->d_wn, p->wn);
-    if (!e) e = dalloc(&p->d_wbase, ne);
-    if (!e) e = dalloc(&p->d_esc_cnt, ne);
-    if (!e) e = dalloc(&p->d_esc_off, ne);
-    if (!e) e = dalloc(&p->d_scan_tmp, ntiles);
-    if (!e) e = dalloc(&p->d_total, 4);
-    if (!e) e = dalloc(&p->d_done, ni);
-    if (!e) e = dalloc(&p->d_counters, 4);
-    if (!e) e = dupload(&p->d_tags, p->tags);
-    if (!e) e = dupload(&p->d_slots, p->slots);
-    if (!e) e = dupload(&p->d_table, p->table);
-    if (!e) e = dupload(&p->d_mixed_items, p->mixed_items);
-    if (!e && getenv("HPEZ_PROFILE")) {
-        e = dalloc(&p->d_prof, 96);
-        if (!e) e = cudaMemset(p->d_prof, 0, 8 * sizeof(unsigned long long));
-        if (!e) e = cudaMemset(p->d_prof + 8, 0xff, 24 * sizeof(unsigned long long));
-        for (int l = 0; l < 12 && !e; l++) e = cudaMemset(p->d_prof + 9 + 2 * l, 0, sizeof(unsigned long long));
-        if (!e) e = cudaMemset(p->d_prof + 32, 0, 64 * sizeof(unsigned long long));
+    if (!p->ws) {  // no caller workspace: one allocation, owned by the plan
+        p->ws_bytes = plan_layout(*p, nullptr);
+        e = cudaMalloc(&p->own_ws, p->ws_bytes);
+        if (e) return cuda_status(e);
+        p->ws = p->own_ws;
     }
-    const size_t nc = std::max<size_t>(p->commits.size(), 1);
-    std::vector<int32_t> clevel(nc, 0);
-    for (size_t i = 0; i < p->commits.size(); i++) clevel[i] = p->commits[i].level;
-    if (!e) e = dupload(&p->d_clevel, clevel);
-    if (!e) e = dalloc(&p->d_cbase, nc);
-    if (!e) e = dalloc(&p->d_cn, nc);
+    plan_layout(*p, (char *)(((uintptr_t)p->ws + 255) & ~(uintptr_t)255));
+    e = up(p->d_commits, p->commits, st);
+    if (!e) e = up(p->d_item_commit, p->item_commit, st);
+    if (!e) e = up(p->d_flow_order, p->flow_order, st);
+    if (!e) e = up(p->d_dep_off, p->dep_off, st);
+    if (!e) e = up(p->d_dep_rng, p->dep_rng, st);
+    if (!e) e = up(p->d_coarse_pairs, p->coarse_pairs, st);
+    if (!e) e = up(p->d_coarse_groups, p->coarse_groups, st);
+    if (!e) e = up(p->d_wn, p->wn, st);
+    if (!e) e = up(p->d_tags, p->tags, st);
+    if (!e) e = up(p->d_slots, p->slots, st);
+    if (!e) e = up(p->d_table, p->table, st);
+    if (!e) e = up(p->d_mixed_items, p->mixed_items, st);
+    if (!e) e = up(p->d_clevel, p->clevel, st);
+    if (!e && p->d_prof) {
+        e = cudaMemsetAsync(p->d_prof, 0, 8 * sizeof(unsigned long long), st);
+        if (!e) e = cudaMemsetAsync(p->d_prof + 8, 0xff, 24 * sizeof(unsigned long long), st);
+        for (int l = 0; l < 12 && !e; l++) e = cudaMemsetAsync(p->d_prof + 9 + 2 * l, 0, sizeof(unsigned long long), st);
+        if (!e) e = cudaMemsetAsync(p->d_prof + 32, 0, 64 * sizeof(unsigned long long), st);
+    }
     if (e) return cuda_status(e);
     SweepArgs A = base_args(*p);
     if (!p->mixed_items.empty()) {
@@ -2240,11 +2235,6 @@ static int plan_setup(Plan *p, cudaStream_t st) {
             p->d_commits, (int)p->commits.size(), p->d_wbase, p->d_wn, p->d_cbase, p->d_cn);
     e = cudaGetLastError();
     if (e) return cuda_status(e);
-    if (p->d.with_stats && p->d.direction == HPEZ_COMPRESS) {
-        e = dalloc(&p->d_csum, nc);
-        if (!e) e = dalloc(&p->d_errbuf, (size_t)std::max<int64_t>(p->num_codes, 1));
-        if (e) return cuda_status(e);
-    }
     p->setup_done = true;
     return HPEZ_OK;
 }
@@ -2274,7 +2264,32 @@ int hpez_plan_create(const hpez_sweep_desc *desc, hpez_plan *out) {
     p.d.block_table = nullptr;
     cudaError_t e = upload_rows();
     if (e) return cuda_status(e);
+    p.profile = getenv("HPEZ_PROFILE") != nullptr;
+    p.clevel.assign(std::max<size_t>(p.commits.size(), 1), 0);
+    for (size_t i = 0; i < p.commits.size(); i++) p.clevel[i] = p.commits[i].level;
+    if (p.d.direction == HPEZ_DECOMPRESS && p.coarse_dsmem && !getenv("HPEZ_NO_FORK")) {
+        // decompress: the zero-count pre-pass runs beside the coarse kernel
+        e = cudaStreamCreateWithFlags(&p.side, cudaStreamNonBlocking);
+        if (!e) e = cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming);
+        if (!e) e = cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming);
+        if (e) return cuda_status(e);
+    }
+    p.ws_bytes = plan_layout(p, nullptr);
     *out = h.release();
+    return HPEZ_OK;
+}
+
+int hpez_plan_workspace_size(hpez_plan plan, int64_t *bytes) {
+    if (!plan || !bytes) return HPEZ_BAD_ARGUMENT;
+    *bytes = (int64_t)plan->p.ws_bytes;
+    return HPEZ_OK;
+}
+
+int hpez_plan_bind_workspace(hpez_plan plan, void *ws, int64_t bytes) {
+    if (!plan || !ws || bytes < (int64_t)plan->p.ws_bytes) return HPEZ_BAD_ARGUMENT;
+    Plan &p = plan->p;
+    if (p.setup_done || p.own_ws) return HPEZ_BAD_ARGUMENT;  // bind once, before the first run
+    p.ws = ws;
     return HPEZ_OK;
 }
 
@@ -2382,9 +2397,9 @@ static int sweep_run(hpez_plan plan, const void *orig, void *work, void *codes, 
     } else if (p.d.direction == HPEZ_COMPRESS && !p.tiles.empty()) {
         // tiled levels recompute halo points from originals that a neighbour
         // may already have overwritten in place: keep a copy
-        if (!p.d_orig_scratch) {
-            cudaError_t e = cudaMalloc(&p.d_orig_scratch, (size_t)p.g.npts * esz);
-            if (e) return cuda_status(e);
+        if (!p.setup_done) {
+            int s = plan_setup(&p, st);
+            if (s) return s;
         }
         cudaError_t e = cudaMemcpyAsync(p.d_orig_scratch, work, (size_t)p.g.npts * esz, cudaMemcpyDeviceToDevice, st);
         if (e) return cuda_status(e);
@@ -2393,7 +2408,8 @@ static int sweep_run(hpez_plan plan, const void *orig, void *work, void *codes, 
     if (p.d.direction == HPEZ_DECOMPRESS && codes_avail < p.num_codes) return HPEZ_CORRUPT_STREAM;
     if (p.num_codes > 0 && !codes) return HPEZ_BAD_ARGUMENT;
     const bool stats = p.d.with_stats && p.d.direction == HPEZ_COMPRESS;
-    if (stats && (!stat_err_sum || !stat_count)) return HPEZ_BAD_ARGUMENT;
+    // stats: err_sum and count together, or neither (dense error grids only)
+    if (stats && (!stat_err_sum) != (!stat_count)) return HPEZ_BAD_ARGUMENT;
     if (!p.setup_done) {
         int s = plan_setup(&p, st);
         if (s) return s;
@@ -2420,15 +2436,9 @@ static int sweep_run(hpez_plan plan, const void *orig, void *work, void *codes, 
     // decompress with the DSMEM coarse kernel: it ranks its own outliers (the
     // coarse levels are the stream prefix), so the zero-count pre-pass only
     // has to finish before the flow kernel and runs on a side stream
-    const bool fork = p.d.direction == HPEZ_DECOMPRESS && p.coarse_dsmem && !getenv("HPEZ_NO_FORK");
+    const bool fork = p.d.direction == HPEZ_DECOMPRESS && p.coarse_dsmem && p.side;
     cudaStream_t pst = st;
     if (fork) {
-        if (!p.side) {
-            e = cudaStreamCreateWithFlags(&p.side, cudaStreamNonBlocking);
-            if (!e) e = cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming);
-            if (!e) e = cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming);
-            if (e) return cuda_status(e);
-        }
         e = cudaEventRecord(p.ev_fork, st);
         if (!e) e = cudaStreamWaitEvent(p.side, p.ev_fork, 0);
         if (e) return cuda_status(e);
@@ -2519,8 +2529,8 @@ static int sweep_run(hpez_plan plan, const void *orig, void *work, void *codes, 
                                                            : gather_outliers_kernel<double, int32_t>);
         gk<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(A, ne, outliers, A.outl_cap);
     }
-    if (stats && !p.commits.empty()) {
-        commit_pairwise_kernel<<<(unsigned)p.commits.size(), 32, 0, st>>>(p.d_errbuf, p.d_cbase, p.d_cn, p.d_csum);
+    if (stats && stat_err_sum && !p.commits.empty()) {
+        commit_pairwise_kernel<<<(unsigned)p.commits.size(), 256, 0, st>>>(p.d_errbuf, p.d_cbase, p.d_cn, p.d_csum);
         stats_accumulate_kernel<<<1, 32, 0, st>>>((int)p.commits.size(), p.d_clevel, p.d_csum, p.d_cn, stat_err_sum,
                                                   stat_count);
     }

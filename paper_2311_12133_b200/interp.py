@@ -90,6 +90,13 @@ class SweepPlan:
         bind()
         check(lib().hpez_plan_create(ctypes.byref(desc), ctypes.byref(h)), "hpez_plan_create")
         self.handle = h
+        # device workspace from torch's caching allocator (the library never
+        # allocates during a run)
+        nb = ctypes.c_int64(0)
+        check(lib().hpez_plan_workspace_size(h, ctypes.byref(nb)), "hpez_plan_workspace_size")
+        self.workspace = torch.empty(max(int(nb.value), 1), dtype=torch.uint8, device=device())
+        check(lib().hpez_plan_bind_workspace(h, ptr(self.workspace), self.workspace.numel()),
+              "hpez_plan_bind_workspace")
         self.n_levels = n_levels
         self.num_codes = int(lib().hpez_plan_num_codes(h))
         self.num_launches = int(lib().hpez_plan_num_launches(h))
@@ -109,7 +116,7 @@ class SweepPlan:
 
 
 _PLANS: "collections.OrderedDict[bytes, SweepPlan]" = collections.OrderedDict()
-_PLAN_CAP = 48
+_PLAN_CAP = 256  # tune() alone builds ~130 trial plans; an LRU smaller than that thrashes
 _PLAN_ENV = ("HPEZ_TILE", "HPEZ_TILE_MIN", "HPEZ_TILE_TY", "HPEZ_TILE_TX", "HPEZ_TILE_ZC", "HPEZ_TILE_NT",
              "HPEZ_COARSE_MAX", "HPEZ_COARSE_CLUSTER", "HPEZ_COARSE_DSMEM")
 

@@ -200,16 +200,21 @@ def run_block_trial(block, bound: float, configs, *, alpha: float = 1.0, beta: f
     alpha_vec = np.ones(len(shape)) if md_alpha is None else np.asarray(md_alpha)
     dev = dblk.orig.device
     nl = len(plan.levels)
-    st = {"err_sum": torch.zeros(nl, dtype=torch.float64, device=dev),
-          "count": torch.zeros(nl, dtype=torch.int64, device=dev),
+    # dense (tune_blocks): only the error grids are read, so the per-commit
+    # err_sum / count reductions are skipped
+    st = {"err_sum": None if dense else torch.zeros(nl, dtype=torch.float64, device=dev),
+          "count": None if dense else torch.zeros(nl, dtype=torch.int64, device=dev),
           "dense": torch.zeros((nl,) + tuple(shape), dtype=torch.float64, device=dev) if dense else None}
     dblk.work.copy_(dblk.orig)
     codes, outl, n_out = run_levels_device(
         dblk.work, plan.levels, direction="compress", radius=radius, frozen_axes=tuple(sorted(frozen)),
         md_alpha=alpha_vec, rounding=rounding, stats=st)
-    err_sum = st["err_sum"].cpu().numpy()
-    count = st["count"].cpu().numpy()
-    mae = np.array([float(err_sum[i] / count[i]) if count[i] else 0.0 for i in range(nl)])
+    if dense:
+        mae = None
+    else:
+        err_sum = st["err_sum"].cpu().numpy()
+        count = st["count"].cpu().numpy()
+        mae = np.array([float(err_sum[i] / count[i]) if count[i] else 0.0 for i in range(nl)])
     codes_np = codes_to_int32(codes) if not dense else None
     mse = rng = math.nan
     if want_work:
