@@ -53,6 +53,14 @@ def histogram_device(codes) -> np.ndarray:
 
 def encode_device(codes):
     """(lengths u8[max+1], payload bytes, nbits) of a device code stream."""
+    lengths, words, nbits = encode_device_words(codes)
+    payload = words.view(torch.uint8)[:(nbits + 7) // 8].cpu().numpy().tobytes()
+    return lengths, payload, nbits
+
+
+def encode_device_words(codes):
+    """(lengths u8[max+1], packed payload as a device int32 tensor, nbits):
+    the payload stays in HBM for the caller to move where it needs it."""
     freqs = histogram_device(codes)
     lengths, values = table(freqs)
     nbits = int((freqs * lengths.astype(np.int64)).sum())
@@ -71,8 +79,7 @@ def encode_device(codes):
     check(lib().hpez_huffman_pack(ptr(codes), cdt, codes.numel(), ptr(ld_t), ptr(vd_t),
                                   int(lengths.max()), ptr(words), nbits, stream()),
           "hpez_huffman_pack")
-    payload = words.view(torch.uint8)[:nbytes].cpu().numpy().tobytes()
-    return lengths, payload, nbits
+    return lengths, words, nbits
 
 
 def encode(symbols):
