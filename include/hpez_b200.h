@@ -194,6 +194,37 @@ int hpez_set_device(int32_t device);
 /* Library build information (arch string) for provenance checks. */
 const char *hpez_build_info(void);
 
+
+/* ---- tuner sampling statistics and quality metrics ----
+ * Reductions follow numpy's pairwise summation bit for bit; `scratch` is
+ * device memory of hpez_reduce_scratch_bytes() bytes, `out` / `sums` are
+ * device doubles.  Grids are f32 (is_f64 = 0) or f64 C-order arrays. */
+int64_t hpez_reduce_scratch_bytes(void);
+/* numpy a.sum() (pairwise) of a device f64 array. */
+int hpez_pairwise_sum(const double *a, int64_t n, double *out, void *scratch, void *stream);
+/* tuner.analyze_samples (tuner.py:86-124): for every axis a in lin_mask /
+ * cub_mask, the pairwise sum of the squared linear / cubic residuals at the
+ * strided interior sample (grid.py:198-219; box lo/size, n samples) into
+ * sums[2a] / sums[2a+1] (divide by n for the reference's np.mean). */
+int hpez_sample_stats(const void *grid, int32_t is_f64, int32_t rank, const int64_t *dims, const int64_t *lo,
+                      const int64_t *size, int64_t n, uint32_t lin_mask, uint32_t cub_mask, double *sums,
+                      void *scratch, void *stream);
+/* metrics.psnr numerator (metrics.py:44-45): pairwise sum of (a - b)^2. */
+int hpez_sq_diff_sum(const void *a, int32_t a_f64, const void *b, int32_t b_f64, int64_t n, double *out,
+                     void *scratch, void *stream);
+/* scipy.ndimage.uniform_filter1d(mode="reflect") of a C-order f64 array
+ * along `axis` (metrics.py:78-82; window <= extent), out of place. */
+int hpez_uniform_filter1d(const double *in, double *out, int32_t rank, const int64_t *dims, int32_t axis,
+                          int32_t size, void *stream);
+/* metrics.ssim operands: x, y, x*x, y*y, x*y as f64 arrays. */
+int hpez_ssim_prep(const void *a, int32_t a_f64, const void *b, int32_t b_f64, int64_t n, double *x, double *y,
+                   double *xx, double *yy, double *xy, void *stream);
+/* metrics.ssim num/den at the centres lo + 2*i (cnt per axis), compact
+ * row-major (metrics.py:83-93). */
+int hpez_ssim_terms(const double *mu_x, const double *mu_y, const double *xx, const double *yy, const double *xy,
+                    int32_t rank, const int64_t *dims, const int64_t *lo, const int64_t *cnt, double c1, double c2,
+                    double *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -224,3 +224,127 @@ def huffman_decode(lengths, payload: bytes, count: int):
     if used < 0:
         raise CorruptStream(f"huffman decode failed ({used})")
     return out
+
+
+# ------------------------------------------------- tuner stats / metrics --
+# numpy restatements (checkers for metrics.cu): same ufunc order as the
+# reference, reductions through numpy itself (pairwise).
+
+_CUBIC = ((-3, -1.0 / 16), (-1, 9.0 / 16), (1, 9.0 / 16), (3, -1.0 / 16))
+
+
+def _reach(extent):  # grid.axis_sampling_reach (grid.py:169-176)
+    return 3 if extent >= 7 else (1 if extent >= 3 else None)
+
+
+def sample_index(dims, rate):
+    """grid.sample_indices (grid.py:179-219): (n, rank) int64."""
+    import math
+    box = [(0, e - 1) if _reach(e) is None else (_reach(e), e - 1 - _reach(e)) for e in dims]
+    sizes = [hi - lo + 1 for lo, hi in box]
+    m = int(np.prod(sizes, dtype=np.int64))
+    n = min(math.ceil(rate * int(np.prod(dims, dtype=np.int64))), m)
+    flat = (np.arange(n, dtype=np.int64) * m) // n
+    out = np.empty((n, len(dims)), dtype=np.int64)
+    for ax in reversed(range(len(dims))):
+        out[:, ax] = flat % sizes[ax] + box[ax][0]
+        flat = flat // sizes[ax]
+    return out
+
+
+def analyze_samples(data, rate=0.002):
+    """tuner.analyze_samples (tuner.py:86-124): (linear_mse, cubic_mse,
+    freeze_candidate, sigma_sq, n)."""
+    import math
+    idx = sample_index(data.shape, rate)
+    vals = data[tuple(idx.T)].astype(np.float64)
+    lin, cub, measured = [], [], []
+    for ax in range(data.ndim):
+        reach = _reach(data.shape[ax])
+        if reach is None:
+            lin.append(math.nan)
+            cub.append(math.nan)
+            continue
+
+        def nb(off, ax=ax):
+            j = idx.copy()
+            j[:, ax] += off
+            return data[tuple(j.T)].astype(np.float64)
+
+        lmse = float(np.mean((vals - 0.5 * (nb(-1) + nb(1))) ** 2))
+        lin.append(lmse)
+        if reach >= 3:
+            pc = sum(c * nb(o) for o, c in _CUBIC)
+            cub.append(float(np.mean((vals - pc) ** 2)))
+        else:
+            cub.append(lmse)
+        measured.append(ax)
+    worst = max((cub[a] for a in measured), default=1.0)
+    sig = [cub[a] if a in measured else max(worst, 1.0) for a in range(data.ndim)]
+    freeze = max(measured, key=lambda a: cub[a])
+    return tuple(lin), tuple(cub), int(freeze), tuple(sig), len(idx)
+
+
+def psnr(x, y):
+    """metrics.psnr (metrics.py:36-51)."""
+    import math
+    x = np.asarray(x).astype(np.float64)
+    y = np.asarray(y).astype(np.float64)
+    mse = float(np.mean((x - y) ** 2))
+    if mse == 0.0:
+        return math.inf
+    rng = float(x.max()) - float(x.min())
+    if rng == 0.0:
+        return None
+    return 20.0 * math.log10(rng) - 10.0 * math.log10(mse)
+
+
+def uniform_filter(x, size):
+    """scipy.ndimage.uniform_filter(x, size) for float64 x, mode 'reflect',
+    size <= extent on every axis: per axis, the running sum of
+    NI_UniformFilter1D (sequential: np.cumsum) divided by the window."""
+    out = x
+    for ax, w in enumerate(size):
+        a = np.moveaxis(out, ax, -1)
+        L = a.shape[-1]
+        s1 = w // 2
+        p = np.arange(-s1, L + (w - s1 - 1))
+        q = np.where(p < 0, -p - 1, np.where(p >= L, 2 * L - p - 1, p))
+        ext = a[..., q]  # reflected line buffer
+        first = np.zeros(a.shape[:-1])
+        for l in range(w):
+            first = first + ext[..., l]
+        d = ext[..., w:w + L - 1] - ext[..., 0:L - 1]
+        run = np.cumsum(np.concatenate([first[..., None], d], axis=-1), axis=-1)
+        out = np.moveaxis(run / w, -1, ax)
+    return np.ascontiguousarray(out)
+
+
+def ssim(a, b):
+    """metrics.ssim (metrics.py:64-94)."""
+    x = np.asarray(a).astype(np.float64)
+    y = np.asarray(b).astype(np.float64)
+    rng = float(x.max()) - float(x.min())
+    scale = rng if rng > 0 else 1.0
+    c1 = (0.01 * scale) ** 2
+    c2 = (0.03 * scale) ** 2
+    win = []
+    for ext in x.shape:
+        w = min(7, ext)
+        if w % 2 == 0:
+            w -= 1
+        win.append(max(w, 1))
+    mu_x = uniform_filter(x, win)
+    mu_y = uniform_filter(y, win)
+    xx = uniform_filter(x * x, win)
+    yy = uniform_filter(y * y, win)
+    xy = uniform_filter(x * y, win)
+    var_x = xx - mu_x * mu_x
+    var_y = yy - mu_y * mu_y
+    cov = xy - mu_x * mu_y
+    sel = tuple(slice(w // 2, ext - (w // 2), 2) for w, ext in zip(win, x.shape))
+    mu_x, mu_y = mu_x[sel], mu_y[sel]
+    var_x, var_y, cov = var_x[sel], var_y[sel], cov[sel]
+    num = (2.0 * mu_x * mu_y + c1) * (2.0 * cov + c2)
+    den = (mu_x ** 2 + mu_y ** 2 + c1) * (var_x + var_y + c2)
+    return float(np.mean(num / den))

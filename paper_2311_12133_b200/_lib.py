@@ -79,6 +79,13 @@ def lib():
         "hpez_huffman_decode": (I32, [P, I64, P, I64, I64, P]),
         "hpez_huffman_decode_device": (I32, [P, P, I64, P, I64, I64, P, I32, P]),
         "hpez_rows_pairwise_sum": (I32, [P, I64, I64, P, P]),
+        "hpez_reduce_scratch_bytes": (I64, []),
+        "hpez_pairwise_sum": (I32, [P, I64, P, P, P]),
+        "hpez_sample_stats": (I32, [P, I32, I32, P, P, P, I64, U32, U32, P, P, P]),
+        "hpez_sq_diff_sum": (I32, [P, I32, P, I32, I64, P, P, P]),
+        "hpez_uniform_filter1d": (I32, [P, P, I32, P, I32, I32, P]),
+        "hpez_ssim_prep": (I32, [P, I32, P, I32, I64, P, P, P, P, P, P]),
+        "hpez_ssim_terms": (I32, [P, P, P, P, P, I32, P, P, P, ctypes.c_double, ctypes.c_double, P, P]),
         "hpez_set_device": (I32, [I32]),
         "hpez_build_info": (ctypes.c_char_p, []),
     }

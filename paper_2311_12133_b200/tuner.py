@@ -27,7 +27,8 @@ from . import _lib
 from ._lib import check, lib
 from .device import bind, device, ptr, stream
 from .errors import GridTooSmall
-from .grid import ScalarGrid, axis_sampling_reach, sample_indices
+from .devgrid import device_grid, reduce_scratch
+from .grid import ScalarGrid, axis_sampling_reach, interior_box
 from .interp import TRAVERSAL_FVFI, codes_to_int32, f32_exact, run_levels_device
 from .plan import (DEFAULT_ANCHOR_STRIDE, KERNEL_VARIANTS, PARADIGM_MULTIDIM, PARADIGM_ONED,
                    CompressionConfig, InterpKernel, KernelTag, LevelConfig, active_axes_of,
@@ -108,41 +109,46 @@ def md_weights(sigma_sq) -> MdWeights:
     return MdWeights(sig, tuple(float(w / total) for w in inv), min(1.0 / total, min(sig)))
 
 
-_CUBIC = ((-3, -1.0 / 16), (-1, 9.0 / 16), (1, 9.0 / 16), (3, -1.0 / 16))
-
-
 def analyze_samples(grid: ScalarGrid, rate: float = 0.002) -> SampleStats:
-    """Per-axis linear / cubic prediction MSE on the strided sample
-    (tuner.py:86-124); numpy ufunc order kept so MSEs are bit-identical."""
-    idx = sample_indices(grid, rate)
-    data = grid.data
-    vals = data[tuple(idx.T)].astype(np.float64)
+    """tuner.analyze_samples (tuner.py:86-124) on the GPU: the strided
+    interior sample (grid.py:198-219) is indexed in the kernel, the squared
+    linear / cubic residuals along every measurable axis are summed in
+    numpy's pairwise order (hpez_sample_stats) and divided by n here, so
+    the MSEs equal the reference's np.mean bit for bit."""
+    if not 0 < rate <= 1:
+        raise ValueError(f"sample rate must be in (0, 1], got {rate}")
+    box = interior_box(grid.dims)  # raises GridTooSmall like the reference
+    sizes = [hi - lo + 1 for lo, hi in box]
+    m = int(np.prod(sizes, dtype=np.int64))
+    n = min(math.ceil(rate * grid.point_count), m)
+    reach = [axis_sampling_reach(e) for e in grid.dims]
+    lin_mask = sum(1 << a for a, r in enumerate(reach) if r is not None)
+    cub_mask = sum(1 << a for a, r in enumerate(reach) if r is not None and r >= 3)
+    g = device_grid(grid)
+    rank = grid.rank
+    dims = np.asarray(grid.dims, dtype=np.int64)
+    lo = np.asarray([b[0] for b in box], dtype=np.int64)
+    sz = np.asarray(sizes, dtype=np.int64)
+    sums = torch.zeros(2 * rank, dtype=torch.float64, device=g.device)
+    bind()
+    check(lib().hpez_sample_stats(ptr(g), int(g.dtype == torch.float64), rank, dims.ctypes.data,
+                                  lo.ctypes.data, sz.ctypes.data, n, lin_mask, cub_mask, ptr(sums),
+                                  ptr(reduce_scratch()), stream()), "hpez_sample_stats")
+    s_h = sums.cpu().numpy()
     lin, cub, measured = [], [], []
-    for ax in range(grid.rank):
-        reach = axis_sampling_reach(grid.dims[ax])
-        if reach is None:
+    for ax in range(rank):
+        if reach[ax] is None:
             lin.append(math.nan)
             cub.append(math.nan)
             continue
-
-        def nb(off, ax=ax):
-            j = idx.copy()
-            j[:, ax] += off
-            return data[tuple(j.T)].astype(np.float64)
-
-        lmse = float(np.mean((vals - 0.5 * (nb(-1) + nb(1))) ** 2))
+        lmse = float(s_h[2 * ax] / n)
         lin.append(lmse)
-        if reach >= 3:
-            # sum() over arrays starts from int 0: 0 + t0 + t1 + ... elementwise
-            pc = sum(c * nb(o) for o, c in _CUBIC)
-            cub.append(float(np.mean((vals - pc) ** 2)))
-        else:
-            cub.append(lmse)
+        cub.append(float(s_h[2 * ax + 1] / n) if reach[ax] >= 3 else lmse)
         measured.append(ax)
     worst = max((cub[a] for a in measured), default=1.0)
-    sig = [cub[a] if a in measured else max(worst, 1.0) for a in range(grid.rank)]
+    sig = [cub[a] if a in measured else max(worst, 1.0) for a in range(rank)]
     freeze = max(measured, key=lambda a: cub[a])
-    return SampleStats(tuple(lin), tuple(cub), int(freeze), tuple(sig), len(idx))
+    return SampleStats(tuple(lin), tuple(cub), int(freeze), tuple(sig), n)
 
 
 def blend_weights_f32(stats: SampleStats) -> tuple:
@@ -174,13 +180,21 @@ def tuning_block(grid: ScalarGrid, extent: int = TUNING_BLOCK_EXTENT) -> np.ndar
 
 class _DeviceBlock:
     """A tuning block resident in HBM with its pristine copy, reused by every
-    trial of one tune() call."""
+    trial of one tune() call.  ``block`` is a host f64 array, or a device
+    tensor already in its working storage (f32 for f32 grids, else f64)."""
 
-    def __init__(self, block: np.ndarray, rounding: int):
+    def __init__(self, block, rounding: int):
         dev = device()
-        self.host = block
-        self.f32 = rounding == ROUND_F32 and f32_exact(block)
-        self.orig = torch.from_numpy(block.astype(np.float32) if self.f32 else block).to(dev)
+        if isinstance(block, torch.Tensor):
+            self.host = None
+            self.shape = tuple(block.shape)
+            self.f32 = block.dtype == torch.float32
+            self.orig = block.contiguous()
+        else:
+            self.host = block
+            self.shape = block.shape
+            self.f32 = rounding == ROUND_F32 and f32_exact(block)
+            self.orig = torch.from_numpy(block.astype(np.float32) if self.f32 else block).to(dev)
         self.work = torch.empty_like(self.orig)
 
 
@@ -192,7 +206,7 @@ def run_block_trial(block, bound: float, configs, *, alpha: float = 1.0, beta: f
     """tuner.run_block_trial (tuner.py:160-185) on the GPU.  ``block`` is a
     host array or a _DeviceBlock; returns the same TrialResult fields."""
     dblk = block if isinstance(block, _DeviceBlock) else _DeviceBlock(np.asarray(block), rounding)
-    shape = dblk.host.shape
+    shape = dblk.shape
     plan = build_level_plan(shape, anchor_stride, bound, alpha, beta, frozen_dim, configs)
     frozen = set(extra_frozen)
     if frozen_dim is not None:
@@ -469,13 +483,15 @@ def tune_blocks(grid: ScalarGrid, global_configs, ebound: float, *,
     starts = [np.arange(c) * bs + lo for c in full_counts]
     mesh = np.meshgrid(*starts, indexing="ij")
     origins = np.stack([m.ravel() for m in mesh], axis=1)
-    # gather the centred sub-blocks (host fancy index, then one upload)
-    idx = [origins[:, a][:, None] + np.arange(sub)[None, :] for a in range(rank)]
+    # gather the centred sub-blocks of every complete block on the device
+    # (the field is already in HBM; values keep their working storage)
+    dg = device_grid(grid)
+    idx = [torch.from_numpy(origins[:, a][:, None] + np.arange(sub)[None, :]).to(dg.device)
+           for a in range(rank)]
     sel = tuple(idx[a].reshape((n_full,) + (1,) * a + (sub,) + (1,) * (rank - 1 - a))
                 for a in range(rank))
-    stacked = grid.data[sel].astype(np.float64)
     rounding = rounding_for_kind(grid.kind)
-    dblk = _DeviceBlock(stacked, rounding)
+    dblk = _DeviceBlock(dg[sel], rounding)
     shifted_active = tuple(1 + a for a in active)
     cands = config_candidates_shifted(active, shifted_active, options)
     alpha_vec = np.concatenate(([0.0], _md_alpha_vec(md_alpha, rank)))

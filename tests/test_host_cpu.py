@@ -16,15 +16,19 @@ def _grid(fx):
 
 
 @pytest.mark.parametrize("fx", fixtures("samples"), ids=lambda f: f.name)
-def test_analyze_samples_matches_reference(fx):
-    from paper_2311_12133_b200.tuner import analyze_samples, blend_weights_f32
+def test_oracle_analyze_samples_matches_reference(fx):
+    """The oracle restatement (the GPU version is checked against the same
+    fixtures in test_metrics_gpu.py)."""
+    from oracle import oracle
+    from paper_2311_12133_b200.tuner import SampleStats, blend_weights_f32
     m = fx.meta
-    st = analyze_samples(_grid(fx), m["rate"])
-    assert np.array_equal(np.array(st.linear_mse), np.array(m["linear_mse"]), equal_nan=True)
-    assert np.array_equal(np.array(st.cubic_mse), np.array(m["cubic_mse"]), equal_nan=True)
-    assert st.freeze_candidate == m["freeze"] and st.n_samples == m["n"]
-    assert list(st.sigma_sq) == m["sigma_sq"]
-    assert list(blend_weights_f32(st)) == m["weights"]
+    g = _grid(fx)
+    lin, cub, freeze, sig, n = oracle.analyze_samples(g.data, m["rate"])
+    assert np.array_equal(np.array(lin), np.array(m["linear_mse"]), equal_nan=True)
+    assert np.array_equal(np.array(cub), np.array(m["cubic_mse"]), equal_nan=True)
+    assert freeze == m["freeze"] and n == m["n"]
+    assert list(sig) == m["sigma_sq"]
+    assert list(blend_weights_f32(SampleStats(lin, cub, freeze, sig, n))) == m["weights"]
 
 
 @pytest.mark.parametrize("fx", fixtures("pipeline"), ids=lambda f: f.name)
