@@ -19,16 +19,17 @@ _ATTR = "_hpez_device_copy"
 def work_dtype(kind: ElementKind):
     """HBM storage of a grid's working values: f32 for f32 grids (every value
     stays f32-representable), f64 otherwise."""
-    return torch.float32 if kind is ElementKind.F32 else torch.float64
+    return torch.float32 if kind.value == ElementKind.F32.value else torch.float64
 
 
 def device_grid(grid: ScalarGrid) -> torch.Tensor:
-    """The grid's values in HBM (f32 or f64, C order), cached on the grid."""
+    """The grid's values in HBM (f32 or f64, C order), cached on the grid.
+    Accepts the reference's ScalarGrid too (matched on ``kind.value``)."""
     t = getattr(grid, _ATTR, None)
     dev = device()
     if t is not None and t.device == dev:
         return t
-    dt = np.float32 if grid.kind is ElementKind.F32 else np.float64
+    dt = np.float32 if grid.kind.value == ElementKind.F32.value else np.float64
     host = np.ascontiguousarray(grid.data, dtype=dt)
     with warnings.catch_warnings():  # read-only host array: torch only reads it
         warnings.simplefilter("ignore", UserWarning)

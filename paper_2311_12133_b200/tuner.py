@@ -1,4 +1,9 @@
-"""Auto-tuning (§6 of the paper) with every trial sweep on the GPU.
+"""REFERENCE RESTATEMENT for the host control flow (candidate lists, scoring, stage
+order of tuner.py:47-579, kept line-for-line equivalent so decisions match); the
+B200 work is the GPU trial sweeps, tune_blocks' device gather + pairwise scoring and
+analyze_samples (csrc/metrics.cu).
+
+Auto-tuning (§6 of the paper) with every trial sweep on the GPU.
 
 Mirrors the reference's tuner.py stage by stage so the chosen configuration
 -- and therefore the archive -- is identical: sampled per-axis statistics
