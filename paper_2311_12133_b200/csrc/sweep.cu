@@ -1067,6 +1067,40 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? HPEZ_FLOW_OCC * 8 / kItem
     }
 }
 
+// Staged levels: every (level, DAG depth) group of the finest levels is one
+// plain data-parallel launch.  The commits of a group never read each other
+// (the depth is the longest path of the commit DAG), and every point they
+// read belongs to an earlier group or level, so launch order is the whole
+// synchronisation: no flags, no CTA barriers and no L1 invalidation.  Warps
+// take (item, warp) units independently, in stream order.
+constexpr int kStageMax = 24;
+struct StageGroup {
+    int32_t n;
+    int32_t c[kStageMax];
+    int32_t u_off[kStageMax + 1];  // unit prefix: n_items * kItemWarps per commit
+};
+
+template <typename T, typename C, int DIR, int ROUND, bool STATS, bool FAST>
+__global__ void __launch_bounds__(kItemThreads, FAST ? HPEZ_FLOW_OCC * 8 / kItemWarps : 3)
+    stage_kernel(const __grid_constant__ SweepArgs A, const __grid_constant__ StageGroup G) {
+    __shared__ CommitDev s_cm[kStageMax];
+    constexpr int W = sizeof(CommitDev) / 4;
+    for (int i = threadIdx.x; i < G.n * W; i += blockDim.x)
+        ((uint32_t *)s_cm)[i] = ((const uint32_t *)&A.commits[G.c[i / W]])[i % W];
+    __syncthreads();
+    const int nw = (int)(gridDim.x * blockDim.x) >> 5;
+    const int total = G.u_off[G.n];
+    int k = 0;
+    for (int u = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < total; u += nw) {
+        while (u >= G.u_off[k + 1]) k++;  // units ascend per warp
+        const CommitDev &cm = s_cm[k];
+        const int local = u - G.u_off[k];
+        const int item = cm.item_base + local / kItemWarps, warp = local % kItemWarps;
+        if (FAST) process_any_fast<T, C, DIR, ROUND>(A, cm, item, warp);
+        else process_warp<T, C, DIR, ROUND, STATS>(A, cm, item, warp);
+    }
+}
+
 // Zero codes of codes[b, b+n), walked by one warp in aligned 16-byte chunks
 // (a few vector loads per lane instead of n/32 dependent scalar rounds).
 // emit(i, r) is called for every zero code with its offset i in the range
@@ -1364,6 +1398,7 @@ static int num_sms() {
     return sms;
 }
 
+constexpr int64_t kStageMinPts = INT64_MAX;  // levels of at least this many points run as staged launches
 constexpr uint32_t kCoarseMax = 20000;  // leading levels of at most this many points (cumulative) run on the coarse cluster (cfg2: levels 0-1; measured sweep, session 2)
 constexpr int kCoarseCluster = 16;
 static int kDiagScale = 16;  // diagonal order: item window width, in units of the dependency reach
@@ -1398,6 +1433,9 @@ struct Plan {
     std::vector<int32_t> wn;   // member count per (item, warp); mixed filled on device
     std::vector<int32_t> mixed_items;
     int32_t c_tile = 0;             // commits [c_tile, n) run as tiled levels (tile.cu)
+    int32_t c_stage = 0;            // commits [c_stage, c_tile) run as staged launches
+    std::vector<StageGroup> stages; // one launch per (level, DAG depth) group
+    bool stage_fast = false;
     std::vector<TilePlan> tiles;    // one per tiled level
     void *d_orig_scratch = nullptr; // originals copy for in-place compress with tiled levels
     std::vector<int> coarse_group;  // (level, depth) group of each coarse commit
@@ -1855,6 +1893,19 @@ struct Plan {
             item += cm.n_items;
         }
         n_items = item;
+        // staged levels: the trailing levels of at least stage_min points each
+        // (HPEZ_STAGE_MIN; the flow kernel keeps the smaller ones)
+        int64_t stage_min = kStageMinPts;
+        if (const char *ev = getenv("HPEZ_STAGE_MIN")) stage_min = atoll(ev);
+        c_stage = c_tile;
+        while (c_stage > c_coarse) {
+            int b = c_stage;
+            const int lvl = commits[b - 1].level;
+            int64_t pts = 0;
+            while (b > 0 && commits[b - 1].level == lvl) pts += commits[--b].npos;
+            if (pts < stage_min || b < c_coarse) break;
+            c_stage = b;
+        }
         // commit DAG
         std::vector<std::vector<int>> preds(nc);
         std::vector<int> depth(nc, 0);
@@ -1933,7 +1984,7 @@ struct Plan {
                 }
                 if (cm.kind != COMMIT_UNIFORM) mixed_items.push_back(gi);
                 dep_off[gi] = (int32_t)dep_rng.size();
-                if (ci >= c_coarse && ci < c_tile) {
+                if (ci >= c_coarse && ci < c_stage) {
                     for (int d : preds[ci])
                         if (d >= c_coarse) dep_rng.push_back(dep_interval(cm, it, commits[d]));
                     const int64_t U = (int64_t)cm.npos / cm.cnt[0];
@@ -1984,16 +2035,39 @@ struct Plan {
             }
             return true;
         };
+        // stage groups: (level, depth) in order, commits of one group independent
+        stages.clear();
+        for (int c = c_stage; c < c_tile;) {
+            int e = c;
+            while (e < c_tile && commits[e].level == commits[c].level) e++;
+            int maxd = 0;
+            for (int k = c; k < e; k++) maxd = std::max(maxd, depth[k]);
+            for (int dd = 0; dd <= maxd; dd++) {
+                StageGroup G{};
+                for (int k = c; k < e; k++) {
+                    if (depth[k] != dd) continue;
+                    if (G.n == kStageMax) {  // split an oversized group (still independent)
+                        stages.push_back(G);
+                        G = StageGroup{};
+                    }
+                    G.c[G.n] = k;
+                    G.u_off[G.n + 1] = G.u_off[G.n] + commits[k].n_items * kItemWarps;
+                    G.n++;
+                }
+                if (G.n) stages.push_back(G);
+            }
+            c = e;
+        }
         flow_order = order_by(true);
         diag_order = valid(flow_order);
         if (!diag_order) flow_order = order_by(false);
         first_flow_item = 0;
         flow_grid = std::max(1, (int)flow_order.size());  // capped by occupancy at launch
-        coarse_fast = flow_fast = true;
+        coarse_fast = flow_fast = stage_fast = true;
         for (int ci = 0; ci < c_tile; ci++) {
             CommitDev &cm = commits[ci];
             cm.fast_id = fast_id_of(cm);
-            bool &f = ci < c_coarse ? coarse_fast : flow_fast;
+            bool &f = ci < c_coarse ? coarse_fast : (ci < c_stage ? flow_fast : stage_fast);
             f = f && cm.fast_id != -1;
         }
         if (getenv("HPEZ_COARSE_GENERIC")) coarse_fast = false;
@@ -2114,8 +2188,11 @@ static int cuda_status(cudaError_t e) {
 
 typedef void (*sweep_fn)(const SweepArgs);
 
+typedef void (*stage_fn)(const SweepArgs, const StageGroup);
+
 struct KernelSet {
     sweep_fn coarse, flow, coarse_fast, flow_fast;  // *_fast null when not instantiated
+    stage_fn stage, stage_fast;
 };
 
 // Fast rank-3 paths are instantiated for the production element types:
@@ -2131,13 +2208,16 @@ static KernelSet pick3(bool stats) {
     if (DIR == HPEZ_COMPRESS && stats) {
         k.coarse = coarse_kernel<T, C, DIR, ROUND, true, false>;
         k.flow = flow_kernel<T, C, DIR, ROUND, true, false>;
+        k.stage = stage_kernel<T, C, DIR, ROUND, true, false>;
         return k;
     }
     k.coarse = coarse_kernel<T, C, DIR, ROUND, false, false>;
     k.flow = flow_kernel<T, C, DIR, ROUND, false, false>;
+    k.stage = stage_kernel<T, C, DIR, ROUND, false, false>;
     if constexpr (kFastTypes<T, C, DIR, ROUND>) {
         k.coarse_fast = coarse_kernel<T, C, DIR, ROUND, false, true>;
         k.flow_fast = flow_kernel<T, C, DIR, ROUND, false, true>;
+        k.stage_fast = stage_kernel<T, C, DIR, ROUND, false, true>;
     }
     return k;
 }
@@ -2307,6 +2387,7 @@ int32_t hpez_plan_num_launches(hpez_plan plan) {
     int n = 0;
     if (!p.coarse_groups.empty()) n++;
     if (!p.flow_order.empty()) n++;
+    n += (int)p.stages.size();
     n += (int)p.tiles.size();
     n += 1;  // escape scan (single-pass look-back kernel)
     n += 1;  // escape count pre-pass (decompress) or outlier gather (compress)
@@ -2504,6 +2585,16 @@ static int sweep_run(hpez_plan plan, const void *orig, void *work, void *codes, 
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kItemThreads, 0) != cudaSuccess || occ < 1) occ = 1;
         const int grid = std::min(p.flow_grid, occ * num_sms());
         f<<<grid, kItemThreads, 0, st>>>(A);
+    }
+    if (!p.stages.empty()) {
+        stage_fn f = (p.stage_fast && ks.stage_fast) ? ks.stage_fast : ks.stage;
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, kItemThreads, 0) != cudaSuccess || occ < 1) occ = 1;
+        for (const StageGroup &G : p.stages) {
+            const int units = G.u_off[G.n];
+            const int grid = std::max(1, std::min((units + kItemWarps - 1) / kItemWarps, occ * num_sms()));
+            f<<<grid, kItemThreads, 0, st>>>(A, G);
+        }
     }
     e = cudaGetLastError();
     if (e) return cuda_status(e);
