@@ -94,155 +94,328 @@ __global__ void __launch_bounds__(128) lorenzo_plane_kernel(const LzGeom g, int6
 }
 
 
-// ---------------------------------------------------------- tile wavefront --
-// Rank <= 3 grids: 8^3 tiles on tile diagonals tz + ty + tx = D.  A tile
-// depends only on tiles of earlier diagonals (every stencil offset is
-// backward and <= 2 < 8), so one warp runs a tile through its 22 internal
-// hyperplanes lz + ly + lx = h (__syncwarp between them) and a grid barrier
-// separates diagonals: 128 global steps on cfg2 instead of 1024 launches.
-// Each warp stages its tile plus the 2-deep backward halo in shared memory.
-constexpr int kLzT = 8;
-constexpr int kLzH = 3 * (kLzT - 1) + 1;
-__constant__ uint16_t c_lt_pts[kLzT * kLzT * kLzT];  // (lz << 6) | (ly << 3) | lx, sorted by h
-__constant__ int16_t c_lt_off[kLzH + 1];
+// ------------------------------------------------------------ pipeline --
+// Rank <= 3 grids, one launch.  CTAs own (y, x) column blocks of kPY x kPX
+// columns and stream z.  Column (ly, lx) handles plane p = t - ly - lx at
+// step t (a 3-D wavefront inside the block: every backward neighbour a
+// point reads was produced at an earlier step, and the points of one step
+// are independent), a CTA barrier separates steps.  Each column keeps its
+// last kPR planes in a shared-memory ring, so a stencil term is one shared
+// load.  Compute threads own kPRows columns each (one point per column per
+// step); the two rows above and columns to the left of the block (owned by
+// the neighbour blocks) enter the same ring through halo threads on the same
+// skewed schedule.  Every global load (originals / codes of the own columns,
+// halo values via ld.cg, i.e. from L2) is issued kPK steps ahead into a
+// register FIFO, so a step costs shared-memory and FP64 latency only.  A
+// halo value may be loaded once the neighbour's published progress covers
+// it: the block above must be kPY + kPK steps ahead, the block to the left
+// kPX + kPK (the diagonal block follows transitively).  Blocks take logical
+// ids from an atomic ticket in launch order, so every block they wait on is
+// already running (no co-residency requirement).  Critical path: about
+// Z + n_block_rows * (kPY + kPK) + n_block_cols * (kPX + kPK) steps, against
+// one launch per hyperplane (Z + Y + X - 2 launches) before.
+constexpr int kPY = 16, kPX = 16, kPR = 16, kPK = 4, kPRows = 1, kPSlack = 8;
+constexpr int kPCompute = (kPY / kPRows) * kPX;                // 256 threads, kPRows columns each
+constexpr int kPHalo = 2 * (kPX + 2) + 2 * kPY;                 // rows -2, -1 (with the corner) + columns -2, -1
+constexpr int kPWork = ((kPCompute + kPHalo + 31) / 32) * 32;  // compute + halo warps
+constexpr int kPPubs = 4;                                       // publisher warps, one per step residue mod 4
+constexpr int kPThreads = kPWork + 32 * kPPubs + 32;            // + publishers + one grant (poller) warp
+constexpr int kPBar = kPWork + 32;                              // named barrier 1 + (t & 3): work warps + one publisher
+constexpr int kPCols = (kPY + 2) * (kPX + 2);
 
-constexpr int kLzS = kLzT + 2;  // staged tile edge: 2-deep backward halo
-constexpr int kLzTileThreads = 128;
+struct LzPipe {
+    int32_t nbx, nblocks;
+    uint32_t *prog;    // per logical block: steps completed + 8 (release / acquire)
+    uint32_t *ticket;
+};
 
-// One point of a staged tile: neighbours from the warp's shared-memory copy
-// sb (origin at tile - 2), reference term order, quantizer as in
-// lorenzo_plane_kernel; the result goes to sb and to the grid.
-template <typename T, typename C, int DIR, int ROUND>
-__device__ __forceinline__ void lz_tile_point(const LzGeom &g, double *sb, int lz, int ly, int lx, int64_t z, int64_t y,
-                                              int64_t x, T *__restrict__ work, C *__restrict__ codes, int64_t code) {
-    const int64_t c[4] = {0, z, y, x};
-    const int so = ((lz + 2) * kLzS + (ly + 2)) * kLzS + (lx + 2);
-    const int64_t i = z * g.estr[1] + y * g.estr[2] + x;
-    if (DIR == HPEZ_DECOMPRESS && code == 0) return;  // outlier already scattered (staged from work)
-    if (DIR == HPEZ_COMPRESS) code = 0;                // escape unless the quantizer accepts
-    double acc = 0.0;
-    for (int t = 0; t < c_lz.n; t++) {
-        bool ok = true;
-#pragma unroll
-        for (int a = 1; a < 4; a++) ok &= c[a] >= c_lz.delta[t][a];
-        if (ok) {
-            const int d = (c_lz.delta[t][1] * kLzS + c_lz.delta[t][2]) * kLzS + c_lz.delta[t][3];
-            acc = __dadd_rn(acc, __dmul_rn(c_lz.coef[t], sb[so - d]));
+// build_stencil (lorenzo.py:24-41) for rank 3 at compile time: the offsets
+// of itertools.product(range(ORDER + 1), repeat=3) minus the origin, in that
+// order, coef = -prod(w[o]).  Lower ranks are padded with leading unit axes:
+// their terms are the dz = 0 (dy = 0) prefix in the same order with the same
+// coefficients, and the in-grid test drops the rest.
+template <int ORDER> struct LzSten;
+template <> struct LzSten<1> {
+    static constexpr int n = 7;
+    __device__ static constexpr int d(int k, int a) {  // k-th offset, axis a (0 z, 1 y, 2 x)
+        return ((k + 1) >> (2 - a)) & 1;
+    }
+    __device__ static constexpr double w(int o) { return o == 0 ? 1.0 : -1.0; }
+    __device__ static constexpr double coef(int k) { return -(w(d(k, 0)) * w(d(k, 1)) * w(d(k, 2))); }
+};
+template <> struct LzSten<2> {
+    static constexpr int n = 26;
+    __device__ static constexpr int d(int k, int a) {
+        return a == 0 ? (k + 1) / 9 : a == 1 ? ((k + 1) / 3) % 3 : (k + 1) % 3;
+    }
+    __device__ static constexpr double w(int o) { return o == 0 ? 1.0 : o == 1 ? -2.0 : 1.0; }
+    __device__ static constexpr double coef(int k) { return -(w(d(k, 0)) * w(d(k, 1)) * w(d(k, 2))); }
+};
+
+// Quantizer of _scan_compress (lorenzo.py:60-88) with the sweep's
+// reciprocal fast path: q = (orig - acc) / 2e is formed as a product and the
+// exact IEEE division decides only when |q| + 0.5 is within 2^-20 of an
+// integer (or huge), so k is always the reference's.
+__device__ __forceinline__ double lz_q(double d, double two_e, double inv) {
+    const double x = __dmul_rn(d, inv);
+    const double y = __dadd_rn(fabs(x), 0.5);
+    const double fl = floor(y);
+    const double fr = __dsub_rn(y, fl);
+    if (fr < 0x1p-20 || fr > 1.0 - 0x1p-20 || y >= 0x1p20) return __ddiv_rn(d, two_e);
+    return x;
+}
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(const int *p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta(int *p, int v) {
+    asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
+template <typename T, typename C, int DIR, int ROUND, int ORDER>
+__global__ void __launch_bounds__(kPThreads, 2) lorenzo_pipe_kernel(const LzGeom g, const LzPipe P,
+                                                                    T *__restrict__ work, C *__restrict__ codes) {
+    using S = LzSten<ORDER>;
+    extern __shared__ __align__(16) unsigned char lz_smem[];
+    T *ring = reinterpret_cast<T *>(lz_smem);  // [kPCols][kPR]
+    __shared__ int s_id, s_done, s_grant;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        s_id = (int)atomicAdd(P.ticket, 1u);
+        s_done = -4;        // = t0: no step complete yet
+        s_grant = -5;       // = t0 - 1: no halo load granted yet
+    }
+    __syncthreads();
+    const int id = s_id;
+    const int by = id / P.nbx, bx = id % P.nbx;
+    const int64_t Z = g.dims[1], Y = g.dims[2], X = g.dims[3];
+    const int64_t y0 = (int64_t)by * kPY, x0 = (int64_t)bx * kPX;
+    const int64_t PS = g.estr[1], RS = g.estr[2];
+    const int t0 = -4, t1 = (int)(Z - 1) + (kPY - 1) + (kPX - 1);  // t0: halo (-2, -2) reaches plane 0
+
+    if (tid >= kPWork && tid < kPWork + 32 * kPPubs) {
+        // publisher warps: warp w joins the step barrier of the steps t = w (mod 4)
+        // only, then releases "t + 1 steps complete" at gpu scope.  The release
+        // fence waits for the CTA's outstanding writes; with four publishers
+        // taking turns it overlaps the next steps instead of stalling them.
+        const int w = (tid - kPWork) >> 5;
+        for (int t = t0 + (((w - t0) % kPPubs) + kPPubs) % kPPubs; t <= t1; t += kPPubs) {
+            named_sync(1 + (t & (kPPubs - 1)), kPBar);
+            if ((tid & 31) == 0) {
+                asm volatile("red.release.gpu.global.max.u32 [%0], %1;" ::"l"(P.prog + id), "r"((uint32_t)(t + 1 + 8))
+                             : "memory");
+                *(volatile int *)&s_done = t + 1;  // monotone hint for the grant warp's look-ahead
+            }
+        }
+        return;
+    }
+    if (tid >= kPWork) {
+        // grant warp (lane 0): lets the halo threads load a plane once the
+        // neighbours' published progress covers it
+        if (tid != kPWork + 32 * kPPubs) return;
+        const uint32_t *prog_up = by > 0 ? P.prog + (id - P.nbx) : nullptr;
+        const uint32_t *prog_left = bx > 0 ? P.prog + (id - 1) : nullptr;
+        const uint32_t fin = (uint32_t)(t1 + 1 + 8);
+        uint32_t seen_up = 0, seen_left = 0;
+        int granted = t0 - 1;
+        while (granted < t1) {
+            const int done = *(volatile int *)&s_done;
+            if (granted < done + kPK + kPSlack) {
+                // halo loads issued at step t read planes up to t + kPK ahead of the schedule
+                const int t = granted + 1;
+                const uint32_t need_up = min((uint32_t)(t + kPK + kPY + 1 + 8), fin);
+                const uint32_t need_left = min((uint32_t)(t + kPK + kPX + 1 + 8), fin);
+                bool ok = true;
+                if (prog_up && seen_up < need_up) ok = (seen_up = ld_acquire(prog_up)) >= need_up;
+                if (ok && prog_left && seen_left < need_left) ok = (seen_left = ld_acquire(prog_left)) >= need_left;
+                if (ok) {
+                    granted = t;
+                    st_release_cta(&s_grant, granted);
+                    continue;
+                }
+            }
+            __nanosleep(20);
+        }
+        return;
+    }
+
+    const bool compute = tid < kPCompute;
+    const int h = tid - kPCompute;
+    const bool halo = !compute && h < kPHalo;
+    int ry = 0, lx = 0, hly = 0;
+    if (compute) {
+        ry = tid / kPX;
+        lx = tid % kPX;
+    } else if (halo) {
+        if (h < 2 * (kPX + 2)) {
+            hly = h / (kPX + 2) - 2;
+            lx = h % (kPX + 2) - 2;
+        } else {
+            const int k = h - 2 * (kPX + 2);
+            hly = k % kPY;
+            lx = k / kPY - 2;
         }
     }
     const int64_t R = g.radius;
-    if (DIR == HPEZ_COMPRESS) {
-        const double orig = sb[so];
-        if (g.bound > 0.0) {
-            const double q = __ddiv_rn(__dsub_rn(orig, acc), g.two_e);
-            double kq = floor(__dadd_rn(fabs(q), 0.5));
-            if (q < 0.0) kq = -kq;
-            if (-(double)R < kq && kq < (double)R) {
-                const double recon = round_native<ROUND>(__dadd_rn(acc, __dmul_rn(g.two_e, kq)));
-                if (fabs(__dsub_rn(recon, orig)) <= g.bound) {
-                    code = (int64_t)kq + R;
-                    sb[so] = recon;
-                    work[i] = (T)recon;
+    const double two_e = g.two_e, inv = two_e > 0.0 ? 1.0 / two_e : 0.0;
+    const int64_t hy = y0 + hly, hx = x0 + lx;
+    const bool h_ok = halo && hy >= 0 && hx >= 0 && hy < Y && hx < X;
+    T *h_ring = ring + (size_t)((hly + 2) * (kPX + 2) + (lx + 2)) * kPR;
+    const int64_t h_ci = hy * RS + hx;
+    int64_t c_y[kPRows];
+    bool c_ok[kPRows];
+#pragma unroll
+    for (int r = 0; r < kPRows; r++) {
+        const int ly = ry + r * (kPY / kPRows);
+        c_y[r] = y0 + ly;
+        c_ok[r] = compute && c_y[r] < Y && x0 + lx < X;
+    }
+    const int64_t cx = x0 + lx;
+    T hf[kPK];
+    T vf[kPRows][kPK];
+    C cf[kPRows][kPK];
+    auto h_plane = [&](int t) { return (int64_t)t - hly - lx; };
+    auto c_plane = [&](int t, int r) { return (int64_t)t - (ry + r * (kPY / kPRows)) - lx; };
+    int grant = t0 - 1;
+    auto await_grant = [&](int t) {  // halo threads: neighbours' planes for step t are final
+        while (grant < t) {
+            grant = ld_acquire_cta(&s_grant);
+            if (grant < t) __nanosleep(20);
+        }
+    };
+    // prologue: planes of steps t0 .. t0 + kPK - 1
+    if (h_ok) await_grant(t0);
+#pragma unroll
+    for (int j = 0; j < kPK; j++) {
+        const int t = t0 + j;
+        if (h_ok) {
+            const int64_t q = h_plane(t);
+            hf[j] = (q >= 0 && q < Z) ? __ldcg(work + q * PS + h_ci) : T(0);
+        }
+#pragma unroll
+        for (int r = 0; r < kPRows; r++) {
+            const int64_t q = c_plane(t, r);
+            const bool ok = c_ok[r] && q >= 0 && q < Z;
+            if (DIR == HPEZ_COMPRESS) vf[r][j] = ok ? work[q * PS + c_y[r] * RS + cx] : T(0);
+            else cf[r][j] = ok ? codes[q * PS + c_y[r] * RS + cx] : C(0);
+        }
+    }
+    // per compute column: grid offset inside a plane, ring base
+    int64_t coff[kPRows];
+    T *cbase[kPRows];
+    bool cedge[kPRows];  // the column touches the grid's y = 0..ORDER-1 or x = 0..ORDER-1 edge
+#pragma unroll
+    for (int r = 0; r < kPRows; r++) {
+        const int ly = ry + r * (kPY / kPRows);
+        coff[r] = c_y[r] * RS + cx;
+        cbase[r] = ring + (size_t)((ly + 2) * (kPX + 2) + (lx + 2)) * kPR;
+        cedge[r] = c_y[r] < ORDER || cx < ORDER;
+    }
+    for (int tb = t0; tb <= t1; tb += kPK) {
+#pragma unroll
+        for (int j = 0; j < kPK; j++) {
+            const int t = tb + j;
+            if (t > t1) break;
+            if (!compute) {  // halo / idle warps (warp-uniform)
+                if (h_ok) {
+                    const int64_t q = h_plane(t);
+                    if (q >= 0 && q < Z) h_ring[q & (kPR - 1)] = hf[j];
+                    const int64_t qn = q + kPK;
+                    if (qn >= 0 && qn < Z) {
+                        await_grant(t);
+                        hf[j] = __ldcg(work + qn * PS + h_ci);
+                    }
+                }
+            } else {
+            // the kPRows points of this thread are independent: their stencil
+            // sums and quantizers are interleaved
+            double acc[kPRows];
+            bool live[kPRows];
+            int pr[kPRows];
+#pragma unroll
+            for (int r = 0; r < kPRows; r++) {
+                pr[r] = (int)c_plane(t, r);
+                live[r] = c_ok[r] && pr[r] >= 0 && pr[r] < Z;
+                acc[r] = 0.0;
+            }
+            // interior warps (every term in the grid for every lane): no per-term test
+            bool inner = true;
+#pragma unroll
+            for (int r = 0; r < kPRows; r++) inner &= !live[r] || (pr[r] >= ORDER && !cedge[r]);
+            if (__all_sync(0xffffffffu, inner)) {
+#pragma unroll
+                for (int k = 0; k < S::n; k++) {
+#pragma unroll
+                    for (int r = 0; r < kPRows; r++) {
+                        const int o = -(S::d(k, 1) * (kPX + 2) + S::d(k, 2)) * kPR;
+                        acc[r] = __dadd_rn(acc[r], __dmul_rn(S::coef(k),
+                                                             (double)cbase[r][o + ((pr[r] - S::d(k, 0)) & (kPR - 1))]));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < S::n; k++) {
+                    const int dz = S::d(k, 0), dy = S::d(k, 1), dx = S::d(k, 2);
+#pragma unroll
+                    for (int r = 0; r < kPRows; r++) {
+                        const double v = (double)cbase[r][-(dy * (kPX + 2) + dx) * kPR + ((pr[r] - dz) & (kPR - 1))];
+                        if (pr[r] >= dz && c_y[r] >= dy && cx >= dx) acc[r] = __dadd_rn(acc[r], __dmul_rn(S::coef(k), v));
+                    }
                 }
             }
-        } else {
-            const double recon = round_native<ROUND>(acc);
-            if (recon == orig) {
-                code = R;
-                sb[so] = recon;
-                work[i] = (T)recon;
-            }
-        }
-        codes[i] = (C)code;
-    } else {
-        const double v = round_native<ROUND>(__dadd_rn(acc, __dmul_rn(g.two_e, (double)(code - R))));
-        sb[so] = v;
-        work[i] = (T)v;
-    }
-}
-
-template <typename T, typename C, int DIR, int ROUND>
-__global__ void __launch_bounds__(kLzTileThreads) lorenzo_tile_kernel(const LzGeom g, T *__restrict__ work,
-                                                                      C *__restrict__ codes, uint32_t *bar) {
-    __shared__ double s_tile[kLzTileThreads / 32][kLzS * kLzS * kLzS];  // one staged tile per warp (8 KB each)
-    __shared__ int32_t s_code[DIR == HPEZ_DECOMPRESS ? kLzTileThreads / 32 : 1][kLzT * kLzT * kLzT];
-    const int64_t Z = g.dims[1], Y = g.dims[2], X = g.dims[3];
-    const int ntz = (int)((Z + kLzT - 1) / kLzT), nty = (int)((Y + kLzT - 1) / kLzT), ntx = (int)((X + kLzT - 1) / kLzT);
-    const int ndiag = ntz + nty + ntx - 2;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    double *sb = s_tile[wib];
-    const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
-    uint32_t target = 0;
-    for (int D = 0; D < ndiag; D++) {
-        const int tz0 = max(0, D - (nty - 1) - (ntx - 1)), tz1 = min(ntz - 1, D);
-        const int npair = (tz1 - tz0 + 1) * nty;
-        for (int k = gw; k < npair; k += nwarps) {
-            const int tz = tz0 + k / nty, ty = k % nty, tx = D - tz - ty;
-            if (tx < 0 || tx >= ntx) continue;
-            const int64_t z0 = (int64_t)tz * kLzT, y0 = (int64_t)ty * kLzT, x0 = (int64_t)tx * kLzT;
-            // stage the tile and its backward halo (earlier diagonals: final)
-            for (int q = lane; q < kLzS * kLzS * kLzS; q += 32) {
-                const int sz = q / (kLzS * kLzS), sy = (q / kLzS) % kLzS, sx = q % kLzS;
-                const int64_t z = z0 - 2 + sz, y = y0 - 2 + sy, x = x0 - 2 + sx;
-                double v = 0.0;
-                if (z >= 0 && y >= 0 && x >= 0 && z < Z && y < Y && x < X)
-                    v = (double)__ldcg(work + z * g.estr[1] + y * g.estr[2] + x);
-                sb[q] = v;
-            }
-            // decompress: the tile's codes, in h order
-            int32_t *sc = s_code[DIR == HPEZ_DECOMPRESS ? wib : 0];
-            if (DIR == HPEZ_DECOMPRESS)
-                for (int q = lane; q < kLzT * kLzT * kLzT; q += 32) {
-                    const int pk = c_lt_pts[q];
-                    const int64_t z = z0 + (pk >> 6), y = y0 + ((pk >> 3) & 7), x = x0 + (pk & 7);
-                    sc[q] = (z < Z && y < Y && x < X) ? (int32_t)__ldcg(codes + z * g.estr[1] + y * g.estr[2] + x) : 0;
+#pragma unroll
+            for (int r = 0; r < kPRows; r++) {
+                const int p = pr[r];
+                const int64_t i = (int64_t)p * PS + coff[r];
+                double v;
+                if (DIR == HPEZ_COMPRESS) {
+                    const double orig = (double)vf[r][j];
+                    int64_t code = 0;
+                    v = orig;
+                    if (g.bound > 0.0) {
+                        const double q = lz_q(__dsub_rn(orig, acc[r]), two_e, inv);
+                        double kq = floor(__dadd_rn(fabs(q), 0.5));
+                        if (q < 0.0) kq = -kq;
+                        const double recon = round_native<ROUND>(__dadd_rn(acc[r], __dmul_rn(two_e, kq)));
+                        if (-(double)R < kq && kq < (double)R && fabs(__dsub_rn(recon, orig)) <= g.bound) {
+                            code = (int64_t)kq + R;
+                            v = recon;
+                        }
+                    } else {
+                        const double recon = round_native<ROUND>(acc[r]);
+                        if (recon == orig) {
+                            code = R;
+                            v = recon;
+                        }
+                    }
+                    if (live[r]) {
+                        if (code != 0) work[i] = (T)v;
+                        codes[i] = (C)code;
+                    }
+                } else {
+                    const int64_t code = (int64_t)cf[r][j];
+                    v = round_native<ROUND>(__dadd_rn(acc[r], __dmul_rn(two_e, (double)(code - R))));
+                    if (live[r]) {
+                        if (code == 0) v = (double)work[i];  // outlier scattered beforehand
+                        else work[i] = (T)v;
+                    }
                 }
-            __syncwarp();
-            for (int h = 0; h < kLzH; h++) {
-#pragma unroll 1
-                for (int q = c_lt_off[h] + lane; q < c_lt_off[h + 1]; q += 32) {
-                    const int pk = c_lt_pts[q];
-                    const int lz = pk >> 6, ly = (pk >> 3) & 7, lx = pk & 7;
-                    const int64_t z = z0 + lz, y = y0 + ly, x = x0 + lx;
-                    if (z < Z && y < Y && x < X)
-                        lz_tile_point<T, C, DIR, ROUND>(g, sb, lz, ly, lx, z, y, x, work, codes,
-                                                        DIR == HPEZ_DECOMPRESS ? (int64_t)sc[q] : 0);
+                if (live[r]) cbase[r][p & (kPR - 1)] = (T)v;
+                const int pn = p + kPK;
+                if (c_ok[r] && pn >= 0 && pn < Z) {
+                    if (DIR == HPEZ_COMPRESS) vf[r][j] = work[(int64_t)pn * PS + coff[r]];
+                    else cf[r][j] = codes[(int64_t)pn * PS + coff[r]];
                 }
-                __syncwarp();
             }
-        }
-        // grid barrier between diagonals (all CTAs co-resident: cooperative launch)
-        __syncthreads();
-        target += gridDim.x;
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(bar, 1u);
-            while (ld_acquire(bar) < target) __nanosleep(32);
-        }
-        __syncthreads();
-    }
-}
-
-static bool lz_tile_table() {
-    static bool done = false;
-    if (done) return true;
-    uint16_t pts[kLzT * kLzT * kLzT];
-    int16_t off[kLzH + 1];
-    int k = 0;
-    for (int h = 0; h < kLzH; h++) {
-        off[h] = (int16_t)k;
-        for (int a = 0; a < kLzT; a++)
-            for (int b = 0; b < kLzT; b++) {
-                const int c = h - a - b;
-                if (c >= 0 && c < kLzT) pts[k++] = (uint16_t)((a << 6) | (b << 3) | c);
             }
+            named_sync(1 + (t & (kPPubs - 1)), kPBar);  // step t complete (ring + global writes), publisher t mod 4
+        }
     }
-    off[kLzH] = (int16_t)k;
-    if (cudaMemcpyToSymbol(c_lt_pts, pts, sizeof pts) != cudaSuccess) return false;
-    if (cudaMemcpyToSymbol(c_lt_off, off, sizeof off) != cudaSuccess) return false;
-    done = true;
-    return true;
 }
 
 template <typename C>
@@ -347,7 +520,7 @@ static int lz_cuda(cudaError_t e) {
 }
 
 template <typename T, typename C>
-static int lorenzo_run(const LzGeom &g, int direction, int rounding, T *work, C *codes, double *outl,
+static int lorenzo_run(const LzGeom &g, int order, int direction, int rounding, T *work, C *codes, double *outl,
                        int64_t outl_cap, int64_t *n_outl, cudaStream_t st) {
     const int64_t nchunks = (g.n + kLzChunk - 1) / kLzChunk;
     uint64_t *cnt = nullptr;
@@ -379,41 +552,34 @@ static int lorenzo_run(const LzGeom &g, int direction, int rounding, T *work, C 
         f = rounding == HPEZ_ROUND_F32 ? lorenzo_plane_kernel<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_F32>
           : rounding == HPEZ_ROUND_INT ? lorenzo_plane_kernel<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_INT>
                                        : lorenzo_plane_kernel<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_NONE>;
-    // opt-in (HPEZ_LORENZO_TILE=1): bit-exact, but measured slower than the
-    // per-hyperplane launches on cfg2 so far (8.0 vs 7.2 ms, order 1)
-    const char *lt = getenv("HPEZ_LORENZO_TILE");
-    bool tiled = g.dims[0] == 1 && lt && atoi(lt) != 0 && lz_tile_table();
-    if (tiled) {
-        typedef void (*tf_t)(const LzGeom, T *, C *, uint32_t *);
-        tf_t tf;
-        if (direction == HPEZ_COMPRESS)
-            tf = rounding == HPEZ_ROUND_F32 ? lorenzo_tile_kernel<T, C, HPEZ_COMPRESS, HPEZ_ROUND_F32>
-               : rounding == HPEZ_ROUND_INT ? lorenzo_tile_kernel<T, C, HPEZ_COMPRESS, HPEZ_ROUND_INT>
-                                            : lorenzo_tile_kernel<T, C, HPEZ_COMPRESS, HPEZ_ROUND_NONE>;
-        else
-            tf = rounding == HPEZ_ROUND_F32 ? lorenzo_tile_kernel<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_F32>
-               : rounding == HPEZ_ROUND_INT ? lorenzo_tile_kernel<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_INT>
-                                            : lorenzo_tile_kernel<T, C, HPEZ_DECOMPRESS, HPEZ_ROUND_NONE>;
-        int occ = 0, dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tf, kLzTileThreads, 0) != cudaSuccess || occ < 1) occ = 1;
-        const int64_t pairs = ((g.dims[1] + kLzT - 1) / kLzT) * ((g.dims[2] + kLzT - 1) / kLzT);
-        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)occ * sms, (pairs + 3) / 4));
-        uint32_t *bar = nullptr;
-        e = cudaMallocAsync((void **)&bar, sizeof(uint32_t), st);
-        if (!e) e = cudaMemsetAsync(bar, 0, sizeof(uint32_t), st);
+    // rank <= 3: one pipelined launch (HPEZ_LORENZO_PIPE=0 selects the
+    // per-hyperplane launches, kept for rank 4 and as a cross-check)
+    const char *lp = getenv("HPEZ_LORENZO_PIPE");
+    bool piped = g.dims[0] == 1 && !(lp && atoi(lp) == 0);
+    if (piped) {
+        typedef void (*pf_t)(const LzGeom, const LzPipe, T *, C *);
+        pf_t pf;
+#define HPEZ_LZP(DIRV, O)                                                                     \
+    (rounding == HPEZ_ROUND_F32 ? lorenzo_pipe_kernel<T, C, DIRV, HPEZ_ROUND_F32, O>          \
+     : rounding == HPEZ_ROUND_INT ? lorenzo_pipe_kernel<T, C, DIRV, HPEZ_ROUND_INT, O>        \
+                                  : lorenzo_pipe_kernel<T, C, DIRV, HPEZ_ROUND_NONE, O>)
+        if (direction == HPEZ_COMPRESS) pf = order == 1 ? HPEZ_LZP(HPEZ_COMPRESS, 1) : HPEZ_LZP(HPEZ_COMPRESS, 2);
+        else pf = order == 1 ? HPEZ_LZP(HPEZ_DECOMPRESS, 1) : HPEZ_LZP(HPEZ_DECOMPRESS, 2);
+#undef HPEZ_LZP
+        LzPipe P{};
+        const int64_t nby = (g.dims[2] + kPY - 1) / kPY;
+        P.nbx = (int32_t)((g.dims[3] + kPX - 1) / kPX);
+        P.nblocks = (int32_t)(nby * P.nbx);
+        e = cudaMallocAsync((void **)&P.prog, sizeof(uint32_t) * ((size_t)P.nblocks + 1), st);
+        if (!e) e = cudaMemsetAsync(P.prog, 0, sizeof(uint32_t) * ((size_t)P.nblocks + 1), st);
         if (e) return lz_cuda(e);
-        LzGeom gg = g;
-        void *args[] = {(void *)&gg, (void *)&work, (void *)&codes, (void *)&bar};
-        e = cudaLaunchCooperativeKernel((const void *)tf, dim3(blocks), dim3(kLzTileThreads), args, 0, st);
-        cudaFreeAsync(bar, st);
-        if (e) {
-            cudaGetLastError();
-            tiled = false;  // cooperative launch unavailable: hyperplane launches
-        }
+        P.ticket = P.prog + P.nblocks;
+        const size_t smem = (size_t)kPCols * kPR * sizeof(T);
+        cudaFuncSetAttribute(pf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        pf<<<(unsigned)P.nblocks, kPThreads, smem, st>>>(g, P, work, codes);
+        cudaFreeAsync(P.prog, st);
     }
-    if (!tiled)
+    if (!piped)
         for (int64_t d = 0; d < planes; d++) f<<<grid, 128, 0, st>>>(g, d, work, codes);
     if (direction == HPEZ_COMPRESS) compact(true);
     e = cudaGetLastError();
@@ -496,10 +662,10 @@ extern "C" int hpez_lorenzo(int32_t rank, const int64_t *dims, int32_t work_dtyp
     const int64_t cap = outliers ? outl_cap : 0;
     if (work_dtype == HPEZ_WORK_F32) {
         if (code_dtype == HPEZ_CODES_U16)
-            return lorenzo_run(g, direction, rounding, (float *)work, (uint16_t *)codes, outliers, cap, n_outliers, st);
-        return lorenzo_run(g, direction, rounding, (float *)work, (int32_t *)codes, outliers, cap, n_outliers, st);
+            return lorenzo_run(g, order, direction, rounding, (float *)work, (uint16_t *)codes, outliers, cap, n_outliers, st);
+        return lorenzo_run(g, order, direction, rounding, (float *)work, (int32_t *)codes, outliers, cap, n_outliers, st);
     }
     if (code_dtype == HPEZ_CODES_U16)
-        return lorenzo_run(g, direction, rounding, (double *)work, (uint16_t *)codes, outliers, cap, n_outliers, st);
-    return lorenzo_run(g, direction, rounding, (double *)work, (int32_t *)codes, outliers, cap, n_outliers, st);
+        return lorenzo_run(g, order, direction, rounding, (double *)work, (uint16_t *)codes, outliers, cap, n_outliers, st);
+    return lorenzo_run(g, order, direction, rounding, (double *)work, (int32_t *)codes, outliers, cap, n_outliers, st);
 }

@@ -8,10 +8,10 @@ from golden import fixtures
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["hyperplanes", "tiles"])
+@pytest.fixture(params=["pipeline", "hyperplanes"])
 def lz_mode(request, monkeypatch):
-    # hyperplane launches (default) and the opt-in tile-wavefront kernel
-    monkeypatch.setenv("HPEZ_LORENZO_TILE", "1" if request.param == "tiles" else "0")
+    # the pipelined single launch (default, rank <= 3) and the per-hyperplane launches
+    monkeypatch.setenv("HPEZ_LORENZO_PIPE", "1" if request.param == "pipeline" else "0")
     return request.param
 
 
