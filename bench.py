@@ -259,10 +259,12 @@ def sweep_bench(P, steps, warmup, dev):
     flush = torch.ones(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     sink = torch.empty(1, dtype=torch.float32, device=dev)
     kw = P.kw
+    t0 = time.perf_counter()
     pc = get_plan(P.dims, P.levels, direction="compress", work_dtype=_lib.WORK_F32,
                   code_dtype=code_dtype_for(kw["radius"]), **kw)
     pd = get_plan(P.dims, P.levels, direction="decompress", work_dtype=_lib.WORK_F32,
                   code_dtype=code_dtype_for(kw["radius"]), **kw)
+    plan_ms = 1e3 * (time.perf_counter() - t0)
     codes = torch.empty(pc.num_codes, dtype=torch.uint16, device=dev)
     outl = torch.empty(pc.num_codes, dtype=torch.float64, device=dev)
 
@@ -287,21 +289,33 @@ def sweep_bench(P, steps, warmup, dev):
         if events:
             events[3].record()
 
-    # correctness gate on the full-size field: exact round trip + bound
-    _, _, n_out = run_levels_device(work.copy_(orig), P.levels, direction="compress", codes=codes,
+    # correctness gate on the full-size field: exact round trip + bound (the
+    # first run also performs the plans' one-time device setup)
+    work.copy_(orig)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, _, n_out = run_levels_device(work, P.levels, direction="compress", codes=codes,
                                     outliers=outl, **kw)
+    first_ms = 1e3 * (time.perf_counter() - t0)
     back.copy_(anchors0)
     run_levels_device(back, P.levels, direction="decompress", codes=codes, outliers=outl, **kw)
     assert torch.equal(back, work), "decompressed grid differs from the compressor's"
     err = float((back.double() - orig.double()).abs().max())
     assert err <= P.eb, f"bound violated: {err} > {P.eb}"
     gate = {"codes": codes.clone(), "outl": outl[:n_out].clone(), "work": work.clone(),
-            "n_out": int(n_out), "max_err": err}
+            "n_out": int(n_out), "max_err": err,
+            "plan": {"host_build_ms": round(plan_ms, 2), "first_compress_ms_incl_setup": round(first_ms, 2),
+                     "commits": int(lib_commits(pc)), "launches_per_sweep": [pc.num_launches, pd.num_launches]}}
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
     return ev, step, gate, pc, pd
+
+
+def lib_commits(plan):
+    from paper_2311_12133_b200 import _lib
+    return _lib.lib().hpez_plan_num_commits(plan.handle)
 
 
 def e2e_bench(P, steps, warmup, dev, n_out, pc):
@@ -528,6 +542,7 @@ def run_b200(args):
                         "stream out and back in, field out), steps pipelined over 3 streams"},
         "gpu_launches": int(args.steps * (pc.num_launches + pd.num_launches)),
         "outliers": gate["n_out"], "max_abs_err": gate["max_err"], "error_bound": P.eb,
+        "plan": gate["plan"],
     }
     line["clocks"] = clk.summary() if rank == 0 else None
     if world > 1 or wl_name == "cfg5":

@@ -1329,18 +1329,27 @@ __global__ void stats_accumulate_kernel(int n_commits, const int32_t *commit_lev
     }
 }
 
-// Per-commit code base and member count from the (item, warp) table.
-__global__ void commit_ranges_kernel(const CommitDev *commits, int nc, const int64_t *wbase, const int32_t *wn,
-                                     int64_t *cbase, int64_t *cn) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+// Per-commit code base and member count from the (item, warp) table: one
+// CTA per commit, block-wide sum of its (item, warp) member counts.
+__global__ void __launch_bounds__(256) commit_ranges_kernel(const CommitDev *commits, int nc, const int64_t *wbase,
+                                                            const int32_t *wn, int64_t *cbase, int64_t *cn) {
+    __shared__ int64_t s_w[8];
+    const int c = blockIdx.x;
     if (c >= nc) return;
     const CommitDev &cm = commits[c];
     const int64_t e0 = (int64_t)cm.item_base * kItemWarps;
     const int64_t e1 = (int64_t)(cm.item_base + cm.n_items) * kItemWarps;
     int64_t n = 0;
-    for (int64_t e = e0; e < e1; e++) n += wn[e];
-    cbase[c] = wbase[e0];
-    cn[c] = n;
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) n += wn[e];
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = n;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += s_w[w];
+        cbase[c] = wbase[e0];
+        cn[c] = t;
+    }
 }
 
 // Out-of-place compress: copy the anchor lattice (multiples of A on every
@@ -2311,7 +2320,7 @@ static int plan_setup(Plan *p, cudaStream_t st) {
     if (p->n_items > 0)
         exclusive_scan(p->d_wn, (int64_t)p->n_items * kItemWarps, p->d_wbase, p->d_scan_tmp, p->d_total, st);
     if (!p->commits.empty())
-        commit_ranges_kernel<<<(unsigned)((p->commits.size() + 127) / 128), 128, 0, st>>>(
+        commit_ranges_kernel<<<(unsigned)p->commits.size(), 256, 0, st>>>(
             p->d_commits, (int)p->commits.size(), p->d_wbase, p->d_wn, p->d_cbase, p->d_cn);
     e = cudaGetLastError();
     if (e) return cuda_status(e);
