@@ -423,7 +423,7 @@ def pipeline_figures(P, dev):
     codes, outl, n_out = run_levels_device(work, P.levels, direction="compress", **P.kw)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    framed = container.pack_codes(codes)
+    framed = container.pack_codes_pinned(codes)  # the pipeline's path (pinned frame, no host copies)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     gpu_s = P.tune_s + (t1 - t0) + (t2 - t1)
@@ -447,6 +447,30 @@ def pipeline_figures(P, dev):
                     "note": "pipeline.compress/decompress: GPU tune + sweep + Huffman, host zlib level 6 "
                             "(libz 1.3, byte-identical archives); zlib streams run on a thread pool"},
     }
+
+
+def e2e_dropin(P, reps=2):
+    """The reference-signature drop-in interp.run_levels(np.ndarray f64, ...)
+    (interp.py:440-445) timed on the headline field: host f64 work in,
+    codes/outliers back as numpy, decompress through a CodeSource, host f64
+    out -- what a caller binding the reference sees."""
+    from paper_2311_12133_b200.interp import CodeSource, run_levels
+    kw = {k: v for k, v in P.kw.items()}
+    best = None
+    for _ in range(reps):
+        work = P.field.astype(np.float64)
+        t0 = time.perf_counter()
+        codes, outl = run_levels(work, P.levels, direction="compress", **kw)
+        back = np.zeros_like(work)
+        back[P.sel] = work[P.sel]
+        run_levels(back, P.levels, direction="decompress", source=CodeSource(codes, outl), **kw)
+        dt = time.perf_counter() - t0
+        assert np.array_equal(back, work)
+        best = dt if best is None else min(best, dt)
+    return {"value": round(P.n * 4 / 1e9 / best, 3), "unit": UNIT, "seconds": round(best, 3),
+            "path": "interp.run_levels drop-in with the reference's numpy f64 arrays (host work in place, "
+                    "int32 codes / f64 outliers returned, CodeSource decompress); includes the f32-exactness "
+                    "scans and the f64<->f32 host conversions"}
 
 
 def eps_sweep(dev, eps_list, steps=3):
@@ -557,6 +581,7 @@ def run_b200(args):
                                           "(oracle/hpez_oracle.c), 1 thread"}
     if rank == 0 and world == 1 and wl_name == "cfg4" and not args.quick:
         line["pipeline"] = pipeline_figures(P, dev)
+        line["e2e_dropin"] = e2e_dropin(P)
         del ev, step, gate
         line["eps_sweep"] = eps_sweep(dev, [1e-2, 1e-3, 1e-4, 1e-5])
         line["cfg2"] = secondary_cfg2(dev, args)

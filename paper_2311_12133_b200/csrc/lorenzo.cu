@@ -207,8 +207,10 @@ __global__ void __launch_bounds__(kPThreads, 2) lorenzo_pipe_kernel(const LzGeom
         for (int t = t0 + (((w - t0) % kPPubs) + kPPubs) % kPPubs; t <= t1; t += kPPubs) {
             named_sync(1 + (t & (kPPubs - 1)), kPBar);
             if ((tid & 31) == 0) {
+#ifndef HPEZ_LZ_NO_PUBLISH
                 asm volatile("red.release.gpu.global.max.u32 [%0], %1;" ::"l"(P.prog + id), "r"((uint32_t)(t + 1 + 8))
                              : "memory");
+#endif
                 *(volatile int *)&s_done = t + 1;  // monotone hint for the grant warp's look-ahead
             }
         }

@@ -86,6 +86,7 @@ class SweepPlan:
 
     def __init__(self, desc: _lib.SweepDesc, n_levels: int, keepalive):
         self._keep = keepalive
+        self._desc = desc  # the descriptor (its arrays live in keepalive)
         h = ctypes.c_void_p()
         bind()
         check(lib().hpez_plan_create(ctypes.byref(desc), ctypes.byref(h)), "hpez_plan_create")

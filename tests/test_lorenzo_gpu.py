@@ -57,3 +57,28 @@ def test_lorenzo_errors():
     with pytest.raises(OutlierUnderflow):
         lorenzo_pass(np.zeros_like(w), 1e-9, 32768, 1, direction="decompress", codes=codes,
                      outliers=outl[:-1])
+
+
+@pytest.mark.parametrize("dims,kind", [((1000,), "f32"), ((37, 53), "f32"), ((17, 40, 33), "f64"),
+                                        ((70, 18, 49), "i32"), ((5, 4, 3, 17), "f32")])
+def test_lorenzo_shapes_vs_oracle(dims, kind, lz_mode):
+    """Ragged extents (not multiples of the 16x16 column blocks), ranks 1-4,
+    f64 and integer grids, both orders, compress and decompress."""
+    from oracle import oracle
+    from paper_2311_12133_b200.lorenzo import lorenzo_pass
+    rng = np.random.default_rng(len(dims) * 7 + dims[0])
+    data = np.cumsum(rng.standard_normal(dims), axis=-1) * 3
+    rounding = {"f32": 1, "f64": 0, "i32": 2}[kind]
+    if kind == "f32":
+        data = data.astype(np.float32).astype(np.float64)
+    elif kind == "i32":
+        data = np.rint(data * 100)
+    for order in (1, 2):
+        a, b = data.copy(), data.copy()
+        ca, oa = oracle.lorenzo(a, 0.05, 32768, order, direction="compress", rounding=rounding)
+        cb, ob = lorenzo_pass(b, 0.05, 32768, order, direction="compress", rounding=rounding)
+        assert np.array_equal(ca, cb) and oa.tobytes() == ob.tobytes() and a.tobytes() == b.tobytes()
+        back = np.zeros_like(data)
+        lorenzo_pass(back, 0.05, 32768, order, direction="decompress", rounding=rounding, codes=cb,
+                     outliers=ob)
+        assert back.tobytes() == b.tobytes()

@@ -136,3 +136,44 @@ def test_sweep_stream_errors():
                    source=CodeSource(codes, outl[:-1]))
     with pytest.raises(ValueError):
         run_levels(w, plan.levels, direction="sideways", radius=32768)
+
+
+@pytest.mark.parametrize("seed,dims,bs", [(11, (70, 66, 90), 16), (12, (65, 130, 33), 8)])
+def test_staged_levels_vs_oracle(seed, dims, bs, monkeypatch):
+    """The opt-in staged execution (one flag-free launch per (level, depth)
+    group, HPEZ_STAGE_MIN) gives the oracle's codes, outliers and
+    reconstruction, uniform and mixed tables alike."""
+    monkeypatch.setenv("HPEZ_STAGE_MIN", "1000")
+    test_sweep_random_tables_vs_oracle(seed, dims, bs, 1)
+
+
+def test_unbound_workspace_plan():
+    """A plan run without a caller-bound workspace allocates one block itself
+    (raw C-ABI use) and produces the same stream."""
+    import ctypes
+    import torch
+    from paper_2311_12133_b200 import _lib
+    from paper_2311_12133_b200.interp import get_plan, run_levels_device, codes_to_int32
+    data, levels, tbl, md = _random_case(21, (40, 44, 48), bs=16, rounding=1)
+    lv = [_Spec(t) for t in levels]
+    f32 = data.astype(np.float32)
+    w1 = torch.from_numpy(f32).cuda()
+    c1, o1, n1 = run_levels_device(w1, lv, direction="compress", radius=32768, md_alpha=md, rounding=1,
+                                   block_size=16, block_table=tbl)
+    plan = get_plan(f32.shape, lv, direction="compress", radius=32768, md_alpha=md, rounding=1,
+                    block_size=16, block_table=tbl, work_dtype=_lib.WORK_F32, code_dtype=_lib.CODES_U16)
+    h = ctypes.c_void_p()  # a second plan from the same descriptor, no workspace bound
+    assert _lib.lib().hpez_plan_create(ctypes.byref(plan._desc), ctypes.byref(h)) == 0
+    w2 = torch.from_numpy(f32).cuda()
+    c2 = torch.empty_like(c1)
+    o2 = torch.empty(c1.numel(), dtype=torch.float64, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    L = _lib.lib()
+    assert L.hpez_sweep_run(h, ctypes.c_void_p(w2.data_ptr()), ctypes.c_void_p(c2.data_ptr()), c2.numel(),
+                            ctypes.c_void_p(o2.data_ptr()), o2.numel(), None, None, None, st) == 0
+    n2 = ctypes.c_int64(0)
+    assert L.hpez_sweep_finish(h, st, ctypes.byref(n2)) == 0
+    L.hpez_plan_destroy(h)
+    assert n2.value == n1
+    assert np.array_equal(codes_to_int32(c2), codes_to_int32(c1))
+    assert torch.equal(w2, w1)
