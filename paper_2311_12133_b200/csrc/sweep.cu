@@ -400,12 +400,9 @@ __device__ __forceinline__ void process_warp(const SweepArgs &A, const CommitDev
                 }
             } else {
                 const int64_t code = (int64_t)codes[ci];
-                if (code != 0) {
-                    const double pred = predict(work, idx, coord, dims, estr, pr, s);
-                    __stcg(work + idx, (T)dequantize_point<ROUND>(pred, code, two_e, R));
-                } else {
-                    esc = true;
-                }
+                const double pred = predict(work, idx, coord, dims, estr, pr, s);  // loads overlap the code load
+                if (code != 0) __stcg(work + idx, (T)dequantize_point<ROUND>(pred, code, two_e, R));
+                else esc = true;
             }
         }
         const uint32_t eb = __ballot_sync(0xffffffffu, esc);
@@ -869,13 +866,12 @@ __device__ __forceinline__ void process_mixed(const SweepArgs &A, const CommitDe
                 esc = c == 0;
                 if (!esc || oop) work[idx] = (T)out;
             } else {
+                // the stencil loads do not wait for the code load (an escape's
+                // prediction is simply discarded)
                 const int64_t code = (int64_t)codes[ci];
-                if (code != 0) {
-                    const double pred = mixed_pred<T>(fid, work, idx, P, s, w0, w1, w2);
-                    work[idx] = (T)dequantize_point<ROUND>(pred, code, two_e, R);
-                } else {
-                    esc = true;
-                }
+                const double pred = mixed_pred<T>(fid, work, idx, P, s, w0, w1, w2);
+                if (code != 0) work[idx] = (T)dequantize_point<ROUND>(pred, code, two_e, R);
+                else esc = true;
             }
         }
         const uint32_t eb = __ballot_sync(0xffffffffu, esc);
