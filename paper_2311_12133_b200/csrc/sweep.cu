@@ -1015,14 +1015,21 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? HPEZ_FLOW_OCC * 8 / kItem
         const long long c1 = A.prof ? clock64() : 0;
         if (warp == 0 && !(A.dbg & 1)) {
             const int k0 = A.dep_off[item], k1 = A.dep_off[item + 1];
-            for (int k = k0; k < k1; k++) {
-                const int2 d = A.dep_rng[k];
-                // acquire loads: no fence instruction, but each invalidates
-                // this SM's L1 (CCTL.IVALL) so the item's plain loads see the
-                // producers' writes; bar.sync below extends it to the CTA
-                for (int q = d.x + lane; q <= d.y; q += 32)
-                    while (ld_acquire(&A.done[q]) == 0) __nanosleep(32);
+            // every dependency flag is polled with relaxed gpu-scope loads in one
+            // pass (independent loads: one L2 round trip, not one per flag);
+            // then a single acquire load invalidates this SM's L1 (CCTL.IVALL)
+            // so the item's plain loads see the producers' writes, and bar.sync
+            // below extends the ordering to the CTA
+            while (true) {
+                bool ok = true;
+                for (int k = k0; k < k1; k++) {
+                    const int2 d = A.dep_rng[k];
+                    for (int q = d.x + lane; q <= d.y; q += 32) ok &= ld_relaxed(&A.done[q]) != 0;
+                }
+                if (__all_sync(0xffffffffu, ok)) break;
+                __nanosleep(32);
             }
+            if (lane == 0 && k1 > k0) (void)ld_acquire(&A.done[A.dep_rng[k0].x]);
         }
         __syncthreads();  // B
         const long long c2 = A.prof ? clock64() : 0;
