@@ -1041,8 +1041,10 @@ __global__ void __launch_bounds__(kItemThreads, FAST ? HPEZ_FLOW_OCC * 8 / kItem
             q_cur = q_next;
             if (q_next < A.n_items) q_next = atomicAdd(A.next, 1);
         }
-        __syncthreads();  // A: CTA writes happen-before thread 0's gpu-scope release
-        if (threadIdx.x == 0) st_release(&A.done[item], 1u);  // cumulative over the CTA's writes
+        __syncthreads();  // A: CTA writes happen-before the gpu-scope release
+        // released from the last warp: its fence overlaps warp 0's polling of
+        // the next item's dependencies instead of delaying it
+        if (threadIdx.x == kItemThreads - 32) st_release(&A.done[item], 1u);  // cumulative over the CTA's writes
         if (A.prof) {
             const long long c3 = clock64();
             t_grab += c1 - c0;
