@@ -69,6 +69,7 @@ def lib():
         "hpez_sweep_run": (I32, [P, P, P, I64, P, I64, P, P, P, P]),
         "hpez_sweep_run_from": (I32, [P, P, P, P, I64, P, I64, P]),
         "hpez_plan_tile_info": (I32, [P, P, I32]),
+        "hpez_plan_row_info": (I32, [P, P]),
         "hpez_sweep_finish": (I32, [P, P, ctypes.POINTER(I64)]),
         "hpez_lorenzo": (I32, [I32, P, I32, P, ctypes.c_double, I64, I32, I32, I32, I32, P,
                                I64, P, I64, ctypes.POINTER(I64), P]),

@@ -34,6 +34,7 @@
 #include "scan.cuh"
 #include "stencil.cuh"
 #include "tile.h"
+#include "row.h"
 
 #ifndef HPEZ_L1_PREFETCH
 #define HPEZ_L1_PREFETCH 0  // measured slower on B200 (kept for experiments)
@@ -1451,6 +1452,7 @@ struct Plan {
     std::vector<StageGroup> stages; // one launch per (level, DAG depth) group
     bool stage_fast = false;
     std::vector<TilePlan> tiles;    // one per tiled level
+    RowPlan rowp;                   // row-fused finest level (row.cu); commits [c_tile, n) when rowp.ok
     void *d_orig_scratch = nullptr; // originals copy for in-place compress with tiled levels
     std::vector<int> coarse_group;  // (level, depth) group of each coarse commit
     CoarsePlan cplan;               // coarse levels in distributed shared memory (coarse.cu)
@@ -2088,6 +2090,32 @@ struct Plan {
     }
     int d_rank() const { return d.rank; }
 
+    // The finest level as row-fused launches (row.cu): rank-3 f32 grids with
+    // u16 codes, no stats, stride 1, multidim variants only, at least
+    // HPEZ_ROW_MIN points (default 1M); HPEZ_ROW=0 keeps it in the flow kernel.
+    void choose_row() {
+        const int nc = (int)commits.size();
+        const char *ev = getenv("HPEZ_ROW");
+        if (ev && atoi(ev) == 0) return;
+        if (d.rank != 3 || d.with_stats || d.work_dtype != HPEZ_WORK_F32 || d.rounding != HPEZ_ROUND_F32 ||
+            d.code_dtype != HPEZ_CODES_U16 || d.frozen_mask || d.direction > HPEZ_DECOMPRESS || nc == 0)
+            return;
+        int64_t min_pts = 1 << 20;
+        if (const char *m = getenv("HPEZ_ROW_MIN")) min_pts = atoll(m);
+        const int li = commits[nc - 1].level;
+        int b = nc;
+        int64_t pts = 0;
+        while (b > 0 && commits[b - 1].level == li) pts += commits[--b].npos;
+        if (pts < min_pts || li != d.n_levels - 1) return;
+        const bool use_tbl = !table.empty();
+        RowPlan rp;
+        if (!row_plan_build(g, &commits[b], &c_vmask[b], nc - b, b, use_tbl ? table.data() + (size_t)li * nblk_table : nullptr,
+                            nblk_table, levels[li].kernel, levels[li].paradigm, level_codes[li], &rp))
+            return;
+        rowp = rp;
+        c_tile = b;
+    }
+
     // Finest levels that run as shared-memory tiled launches (tile.cu):
     // rank-3 f32 grids with u16 codes, no stats, uniform commits, at least
     // HPEZ_TILE_MIN points (default 200k).  `final` builds the real plans
@@ -2096,6 +2124,7 @@ struct Plan {
         const int nc = (int)commits.size();
         if (final) {
             tiles.clear();
+            if (rowp.ok) return;
             for (int c = c_tile; c < nc;) {
                 int e = c;
                 while (e < nc && commits[e].level == commits[c].level) e++;
@@ -2107,6 +2136,9 @@ struct Plan {
             return;
         }
         c_tile = nc;
+        rowp = RowPlan{};
+        choose_row();
+        if (rowp.ok) return;
         // opt-in (HPEZ_TILE=1): measured slower than the flow kernel on cfg2
         // so far (profiles/); kept parity-green for the tiling work ahead
         const char *ev = getenv("HPEZ_TILE");
@@ -2180,6 +2212,12 @@ static size_t plan_layout(Plan &p, char *base) {
         c.take(&p.d_errbuf, (size_t)std::max<int64_t>(p.num_codes, 1));
     }
     if (p.profile) c.take(&p.d_prof, 96);
+    if (p.rowp.ok) {
+        c.take(&p.rowp.d_cnt, (size_t)p.rowp.d.n_entries);
+        c.take(&p.rowp.d_base, (size_t)p.rowp.d.n_entries);
+        c.take(&p.rowp.d_tmp, (size_t)scan_tmp_size(p.rowp.d.n_entries));
+        c.take(&p.rowp.d_total, 4);
+    }
     if (!p.tiles.empty() && p.d.direction == HPEZ_COMPRESS) {
         char *o;
         c.take(&o, (size_t)p.g.npts * (p.d.work_dtype == HPEZ_WORK_F32 ? 4 : 8));
@@ -2328,6 +2366,8 @@ static int plan_setup(Plan *p, cudaStream_t st) {
         commit_ranges_kernel<<<(unsigned)p->commits.size(), 256, 0, st>>>(
             p->d_commits, (int)p->commits.size(), p->d_wbase, p->d_wn, p->d_cbase, p->d_cn);
     e = cudaGetLastError();
+    if (!e && p->rowp.ok)
+        e = row_plan_setup(p->rowp, p->table.empty() ? nullptr : p->d_table + (size_t)(p->d.n_levels - 1) * p->nblk_table, st);
     if (e) return cuda_status(e);
     p->setup_done = true;
     return HPEZ_OK;
@@ -2624,6 +2664,28 @@ static int sweep_run(hpez_plan plan, const void *orig, void *work, void *codes, 
             if (e) return cuda_status(e);
         }
     }
+    if (p.rowp.ok) {
+        const int64_t e0 = (int64_t)p.commits[p.c_tile].item_base * kItemWarps;
+        if (p.d.direction == HPEZ_COMPRESS) {
+            e = cudaMemsetAsync(p.d_esc_cnt + e0, 0, (size_t)(ne - e0) * sizeof(uint32_t), st);
+            if (e) return cuda_status(e);
+        }
+        RowRun rr{};
+        rr.orig = (const float *)orig;
+        rr.work = (float *)work;
+        rr.codes = (uint16_t *)codes;
+        rr.outl = outliers;
+        rr.outl_cap = A.outl_cap;
+        rr.esc_cnt = p.d_esc_cnt;
+        rr.esc_off = p.d_esc_off;
+        rr.flags = p.d_counters + 1;
+        rr.table = p.table.empty() ? nullptr : p.d_table + (size_t)(p.d.n_levels - 1) * p.nblk_table;
+        rr.rowbase = p.rowp.d_base;
+        rr.commits = p.d_commits;
+        rr.wbase = p.d_wbase;
+        e = row_plan_launch(p.rowp, p.d.direction, rr, st);
+        if (e) return cuda_status(e);
+    }
     if (p.d.direction == HPEZ_COMPRESS) {
         exclusive_scan(p.d_esc_cnt, ne, p.d_esc_off, p.d_scan_tmp, p.d_total, st);
         const int64_t thr = (ne + 31) / 32 * 32;
@@ -2667,6 +2729,18 @@ int hpez_plan_tile_info(hpez_plan plan, int64_t *out, int32_t cap) {
         for (int i = 0; i < 8 && k < cap; i++) out[k++] = v[i];
         c += t.d.n_commits;
     }
+    return HPEZ_OK;
+}
+
+int hpez_plan_row_info(hpez_plan plan, int64_t *out) {
+    if (!plan || !out) return HPEZ_BAD_ARGUMENT;
+    const Plan &p = plan->p;
+    out[0] = p.rowp.ok ? 1 : 0;
+    out[1] = p.rowp.ok ? p.c_tile : -1;
+    out[2] = p.rowp.n_launch;
+    out[3] = p.rowp.d.n_entries;
+    out[4] = p.rowp.d.any_same;
+    out[5] = (int64_t)p.rowp.smem;
     return HPEZ_OK;
 }
 

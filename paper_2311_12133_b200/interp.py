@@ -119,7 +119,8 @@ class SweepPlan:
 _PLANS: "collections.OrderedDict[bytes, SweepPlan]" = collections.OrderedDict()
 _PLAN_CAP = 256  # tune() alone builds ~130 trial plans; an LRU smaller than that thrashes
 _PLAN_ENV = ("HPEZ_TILE", "HPEZ_TILE_MIN", "HPEZ_TILE_TY", "HPEZ_TILE_TX", "HPEZ_TILE_ZC", "HPEZ_TILE_NT",
-             "HPEZ_COARSE_MAX", "HPEZ_COARSE_CLUSTER", "HPEZ_COARSE_DSMEM")
+             "HPEZ_COARSE_MAX", "HPEZ_COARSE_CLUSTER", "HPEZ_COARSE_DSMEM", "HPEZ_ROW", "HPEZ_ROW_MIN",
+             "HPEZ_STAGE_MIN")
 
 
 def _level_array(levels, rank):

@@ -1,0 +1,195 @@
+"""GPU parity of the row-fused finest level (csrc/row.cu) against the CPU oracle.
+
+The finest level of these rank-3 f32 plans is forced onto the row path
+(HPEZ_ROW_MIN=0): every multidim kernel variant as a uniform level, mixed
+per-block tables over the multidim variants with several block sizes, grids
+whose extents are not multiples of the chunk / block / 4-row phases, tiny
+error bounds (many escapes, both directions), the out-of-place compress
+entry, and the fallbacks (x extent not a multiple of 4, one-axis variants)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+class _Spec:
+    def __init__(self, t):
+        from paper_2311_12133_b200.plan import (KERNEL_VARIANTS, PARADIGM_MULTIDIM,
+                                                PARADIGM_ONED, LevelConfig)
+        stride, bound, k, par, order = t
+        self.stride, self.bound = stride, bound
+        self.config = LevelConfig(KERNEL_VARIANTS[k], PARADIGM_MULTIDIM if par else PARADIGM_ONED,
+                                  None if order is None else tuple(order))
+
+
+def _levels(seed, anchor, e, finest_kernel, finest_par=1):
+    rng = np.random.default_rng(seed)
+    out = []
+    n = anchor.bit_length() - 1
+    for i in range(n):
+        last = i == n - 1
+        k = finest_kernel if last else int(rng.integers(0, 5))
+        p = finest_par if last else int(rng.integers(0, 2))
+        order = tuple(int(a) for a in rng.permutation(3)) if p == 0 else None
+        s = anchor >> (i + 1)
+        out.append((s, e / min(1.5 ** (s.bit_length() - 1), 3.0), k, p, order))
+    return out
+
+
+def _table(seed, dims, bs, nl, finest_tags):
+    from paper_2311_12133_b200.plan import order_candidates
+    rng = np.random.default_rng(seed + 1000)
+    tags = [p * 8 + k for p in range(len(order_candidates((0, 1, 2))) + 1) for k in range(5)]
+    nb = int(np.prod([-(-d // bs) for d in dims]))
+    tbl = np.array(tags, np.uint8)[rng.integers(0, len(tags), (nl, nb))]
+    tbl[nl - 1] = np.array(finest_tags, np.uint8)[rng.integers(0, len(finest_tags), nb)]
+    return tbl
+
+
+def _field(dims):
+    import synthetic as syn
+    return syn.config_field(2, dims=dims).astype(np.float32)
+
+
+def _row_info(shape, levels, md, bs=0, tbl=None):
+    from paper_2311_12133_b200 import _lib
+    from paper_2311_12133_b200.interp import code_dtype_for, get_plan
+    lv = [_Spec(t) for t in levels]
+    plan = get_plan(tuple(shape), lv, direction="compress", radius=32768, md_alpha=md, rounding=1,
+                    block_size=bs, block_table=tbl, work_dtype=_lib.WORK_F32,
+                    code_dtype=code_dtype_for(32768))
+    buf = (ctypes.c_int64 * 8)()
+    assert _lib.lib().hpez_plan_row_info(plan.handle, buf) == 0
+    return list(buf)
+
+
+def _roundtrip(data, levels, md, bs=0, tbl=None, oop=False):
+    import torch
+
+    from paper_2311_12133_b200.interp import codes_to_int32, run_levels_device
+    lv = [_Spec(t) for t in levels]
+    kw = dict(radius=32768, md_alpha=md, rounding=1, block_size=bs, block_table=tbl)
+    ref = data.astype(np.float64)
+    c_o, o_o = oracle.run_levels(ref, levels, direction="compress", **kw)
+    src = torch.from_numpy(data).cuda()
+    if oop:
+        work = torch.full_like(src, float("nan"))
+        codes, outl, n_out = run_levels_device(work, lv, direction="compress", orig=src, **kw)
+        assert torch.equal(src.cpu(), torch.from_numpy(data)), "orig was modified"
+    else:
+        work = src
+        codes, outl, n_out = run_levels_device(work, lv, direction="compress", **kw)
+    c_g = codes_to_int32(codes)
+    bad = np.flatnonzero(c_g != c_o)
+    assert bad.size == 0, f"{bad.size} codes differ, first at {bad[:5]} of {c_o.size}"
+    assert outl[:n_out].cpu().numpy().tobytes() == o_o.tobytes(), "outliers differ"
+    assert np.array_equal(work.cpu().numpy().astype(np.float64), ref), "reconstruction differs"
+    back = torch.zeros_like(work)
+    back[::64, ::64, ::64] = work[::64, ::64, ::64]
+    used = run_levels_device(back, lv, direction="decompress", codes=codes,
+                             outliers=outl[:max(n_out, 1)], **kw)
+    assert used == n_out
+    assert torch.equal(back, work), "decompression differs"
+    return n_out
+
+
+@pytest.fixture(autouse=True)
+def _force_rows(monkeypatch):
+    monkeypatch.setenv("HPEZ_ROW_MIN", "0")
+    from paper_2311_12133_b200 import interp
+    if hasattr(interp, "_PLANS"):
+        interp._PLANS.clear()
+
+
+UNIFORM = [
+    # seed, dims, finest kernel variant
+    (1, (70, 66, 92), 0),
+    (2, (65, 130, 36), 1),
+    (3, (129, 100, 56), 2),
+    (4, (40, 77, 140), 3),
+    (5, (96, 64, 64), 4),
+    (6, (33, 97, 260), 4),
+    (7, (9, 10, 12), 2),
+    (8, (67, 69, 128), 0),
+    (9, (66, 71, 132), 4),
+]
+
+
+@pytest.mark.parametrize("seed,dims,kernel", UNIFORM)
+def test_row_uniform_vs_oracle(seed, dims, kernel):
+    data = _field(dims)
+    e = 1e-3 * float(data.max() - data.min())
+    levels = _levels(seed, 64, e, kernel)
+    md = np.random.default_rng(seed).uniform(0, 1, 3)
+    assert _row_info(data.shape, levels, md)[0] == 1
+    _roundtrip(data, levels, md)
+
+
+MIXED = [
+    # seed, dims, block size, finest tags
+    (11, (70, 66, 92), 16, (0, 1, 2, 3, 4)),
+    (12, (65, 130, 36), 32, (0, 1, 2, 3, 4)),
+    (13, (129, 100, 56), 8, (0, 2)),
+    (14, (40, 77, 140), 4, (0, 1, 3)),
+    (15, (96, 64, 64), 32, (0, 4)),
+    (16, (67, 69, 260), 16, (2, 4)),
+    (17, (97, 64, 128), 32, (0, 1, 2, 3, 4)),
+    (18, (66, 130, 132), 32, (0, 1, 2, 3)),
+]
+
+
+@pytest.mark.parametrize("seed,dims,bs,tags", MIXED)
+def test_row_mixed_vs_oracle(seed, dims, bs, tags):
+    data = _field(dims)
+    e = 1e-3 * float(data.max() - data.min())
+    levels = _levels(seed, 64, e, 0)
+    tbl = _table(seed, dims, bs, len(levels), tags)
+    md = np.random.default_rng(seed).uniform(0, 1, 3)
+    assert _row_info(data.shape, levels, md, bs, tbl)[0] == 1
+    _roundtrip(data, levels, md, bs, tbl)
+
+
+@pytest.mark.parametrize("seed,dims,bs", [(21, (70, 66, 92), 0), (22, (45, 81, 64), 16)])
+def test_row_out_of_place(seed, dims, bs):
+    data = _field(dims)
+    e = 1e-3 * float(data.max() - data.min())
+    levels = _levels(seed, 64, e, 4)
+    tbl = _table(seed, dims, bs, len(levels), (0, 1, 2, 3, 4)) if bs else None
+    md = np.array([0.2, 0.5, 0.3])
+    _roundtrip(data, levels, md, bs, tbl, oop=True)
+
+
+@pytest.mark.parametrize("seed,dims,eps,bs", [(31, (70, 66, 92), 1e-6, 0), (32, (48, 52, 60), 1e-9, 16),
+                                              (33, (66, 70, 132), 1e-5, 32)])
+def test_row_escapes(seed, dims, eps, bs):
+    rng = np.random.default_rng(seed)
+    data = (_field(dims) + rng.standard_normal(dims).astype(np.float32) * 0.3).astype(np.float32)
+    e = eps * float(data.max() - data.min())
+    levels = _levels(seed, 64, e, 4)
+    tbl = _table(seed, dims, bs, len(levels), (0, 1, 2, 3, 4)) if bs else None
+    md = np.array([0.3, 0.3, 0.4])
+    n_out = _roundtrip(data, levels, md, bs, tbl)
+    assert n_out > 300
+
+
+def test_row_fallbacks():
+    """Ineligible finest levels stay in the flow kernel and still match."""
+    md = np.array([0.3, 0.3, 0.4])
+    data = _field((40, 44, 50))  # x extent not a multiple of 4
+    e = 1e-3 * float(data.max() - data.min())
+    levels = _levels(41, 64, e, 0)
+    assert _row_info(data.shape, levels, md)[0] == 0
+    _roundtrip(data, levels, md)
+    data = _field((40, 44, 48))
+    levels = _levels(42, 64, e, 3, finest_par=0)  # one-axis paradigm at the finest level
+    assert _row_info(data.shape, levels, md)[0] == 0
+    _roundtrip(data, levels, md)
+    levels = _levels(43, 64, e, 0)
+    tbl = _table(43, data.shape, 16, len(levels), (0, 9, 18))  # one-axis tags in the finest table
+    assert _row_info(data.shape, levels, md, 16, tbl)[0] == 0
+    _roundtrip(data, levels, md, 16, tbl)
