@@ -183,10 +183,10 @@ int hpez_plan_info(hpez_plan plan, int64_t *out);
  * commits written (at most cap / 6) or a negative status. */
 int32_t hpez_plan_commit_stats(hpez_plan plan, int64_t *out, int32_t cap);
 
-/* Diagnostics: out[0] = 1 when the finest level runs as row-fused launches
- * (csrc/row.cu: interp.run_level at stride 1, interp.py:415-433), out[1] its
- * first commit, out[2] launches, out[3] row-base entries, out[4] same-level
- * variant present, out[5] dynamic shared memory per CTA. */
+/* Diagnostics: out[0] = number of fine levels that run as row-fused launches
+ * (csrc/row.cu: interp.run_level at strides 1, 2, 4, interp.py:415-433),
+ * out[1] their first commit, out[2] launches, out[3] row-base entries,
+ * out[4] same-level variant present, out[5] dynamic shared memory per CTA. */
 int hpez_plan_row_info(hpez_plan plan, int64_t *out);
 
 /* HPEZ_PROFILE plans only: out[0..24) per-level (first item start, last

@@ -1,4 +1,4 @@
-// row.h -- row-fused finest level of the rank-3 sweep (row.cu), host
+// row.h -- row-fused fine levels of the rank-3 sweep (row.cu), host
 // interface used by the sweep planner (sweep.cu).
 //
 // The finest level (stride 1) of a multidim configuration holds 7/8 of a
@@ -21,10 +21,12 @@ namespace hpez {
 // Classes of a rank-3 level in reference order (interp.py:417-418):
 // 0 (z)  1 (y)  2 (x)  3 (z,y)  4 (z,x)  5 (y,x)  6 (z,y,x).
 struct RowDesc {
-    int32_t L[3];
-    int32_t E0, E1;              // element strides of z and y
-    int32_t has_table, const_k;  // block table present / the level's kernel variant when not
-    int32_t bsh, bs0, bs1;       // log2(block size), block-grid strides of z and y
+    int32_t L[3];                // lattice extents of the level (coordinates / s)
+    int32_t s;                   // level stride
+    int32_t E0, E1;              // element strides of one lattice step along z and y
+    int32_t has_table, const_tag;  // block table present / the level's tag (plan.encode_tag) when not
+    int32_t bsh, bs0, bs1;       // log2(block size in lattice units), block-grid strides of z and y
+    uint32_t oned_sel[7];        // per class: term index used by one-axis order p, 4 bits each
     int32_t any_same;            // some block of the level uses a same-level variant
     int32_t R;
     int32_t cny[2];              // class rows along y for y-even / y-odd rows
@@ -76,14 +78,14 @@ struct RowPlan {
     int threads = 0;
 };
 
-// Builds the row plan of the finest level from its commits (reference
-// order).  `tbl` is the level's host block table (or null).  False when the
-// level is not eligible: rank != 3, stride != 1, x extent not a multiple of
-// 4, a one-axis (oned) variant on a class of two or more axes, block size
-// below 4 or not a power of two.
+// Builds the row plan of one level (stride 1, 2 or 4) from its commits
+// (reference order).  `tbl` is the level's host block table (or null, then
+// `level_tag` is the level's own tag).  False when the level is not
+// eligible: rank != 3, lattice x extent not a multiple of 4, a one-axis
+// (oned) variant with a same-level split, blocks smaller than four lattice
+// points or not a power of two.
 bool row_plan_build(const GridDev &g, const CommitDev *cms, const uint32_t *vmask, int n, int first_commit,
-                    const uint8_t *tbl, int64_t nblk, int level_kernel, int level_paradigm, int64_t level_base,
-                    RowPlan *out);
+                    const uint8_t *tbl, int64_t nblk, int level_tag, int64_t level_base, RowPlan *out);
 // Row-base table: member counts per (class, pass, row) and their exclusive scan.
 cudaError_t row_plan_setup(RowPlan &p, const uint8_t *d_table_level, cudaStream_t st);
 cudaError_t row_plan_launch(const RowPlan &p, int dir, const RowRun &r, cudaStream_t st);

@@ -1452,7 +1452,8 @@ struct Plan {
     std::vector<StageGroup> stages; // one launch per (level, DAG depth) group
     bool stage_fast = false;
     std::vector<TilePlan> tiles;    // one per tiled level
-    RowPlan rowp;                   // row-fused finest level (row.cu); commits [c_tile, n) when rowp.ok
+    std::vector<RowPlan> rows;      // row-fused fine levels (row.cu), coarse to fine; commits [c_tile, n) when non-empty
+    std::vector<int> row_level;     // level index of each row plan
     void *d_orig_scratch = nullptr; // originals copy for in-place compress with tiled levels
     std::vector<int> coarse_group;  // (level, depth) group of each coarse commit
     CoarsePlan cplan;               // coarse levels in distributed shared memory (coarse.cu)
@@ -2090,9 +2091,10 @@ struct Plan {
     }
     int d_rank() const { return d.rank; }
 
-    // The finest level as row-fused launches (row.cu): rank-3 f32 grids with
-    // u16 codes, no stats, stride 1, multidim variants only, at least
-    // HPEZ_ROW_MIN points (default 1M); HPEZ_ROW=0 keeps it in the flow kernel.
+    // The finest levels as row-fused launches (row.cu): rank-3 f32 grids with
+    // u16 codes, no stats, strides 1 / 2 / 4, multidim or split-free one-axis
+    // variants, at least HPEZ_ROW_MIN points each (default 1M);
+    // HPEZ_ROW=0 keeps them in the flow kernel, HPEZ_ROW_LEVELS caps how many.
     void choose_row() {
         const int nc = (int)commits.size();
         const char *ev = getenv("HPEZ_ROW");
@@ -2102,18 +2104,39 @@ struct Plan {
             return;
         int64_t min_pts = 1 << 20;
         if (const char *m = getenv("HPEZ_ROW_MIN")) min_pts = atoll(m);
-        const int li = commits[nc - 1].level;
-        int b = nc;
-        int64_t pts = 0;
-        while (b > 0 && commits[b - 1].level == li) pts += commits[--b].npos;
-        if (pts < min_pts || li != d.n_levels - 1) return;
+        int max_levels = 3;
+        if (const char *m = getenv("HPEZ_ROW_LEVELS")) max_levels = atoi(m);
         const bool use_tbl = !table.empty();
-        RowPlan rp;
-        if (!row_plan_build(g, &commits[b], &c_vmask[b], nc - b, b, use_tbl ? table.data() + (size_t)li * nblk_table : nullptr,
-                            nblk_table, levels[li].kernel, levels[li].paradigm, level_codes[li], &rp))
-            return;
-        rowp = rp;
-        c_tile = b;
+        const auto oc = order_candidates();
+        int e = nc;
+        while (e > 0 && (int)rows.size() < max_levels) {
+            const int li = commits[e - 1].level;
+            int b = e;
+            int64_t pts = 0;
+            while (b > 0 && commits[b - 1].level == li) pts += commits[--b].npos;
+            if (pts < min_pts) break;
+            // the level's own tag (plan.encode_tag, plan.py:69-75) when there is no table
+            int tag = levels[li].kernel;
+            if (levels[li].paradigm != 1) {
+                int pi = -1;
+                for (size_t k = 0; k < oc.size(); k++) {
+                    bool same = (int)oc[k].size() == levels[li].n_order;
+                    for (int j = 0; same && j < levels[li].n_order; j++) same = oc[k][j] == levels[li].axis_order[j];
+                    if (same) pi = (int)k;
+                }
+                if (pi < 0) break;
+                tag += 8 * (pi + 1);
+            }
+            RowPlan rp;
+            if (!row_plan_build(g, &commits[b], &c_vmask[b], e - b, b,
+                                use_tbl ? table.data() + (size_t)li * nblk_table : nullptr, nblk_table, tag,
+                                level_codes[li], &rp))
+                break;
+            rows.insert(rows.begin(), rp);
+            row_level.insert(row_level.begin(), li);
+            c_tile = b;
+            e = b;
+        }
     }
 
     // Finest levels that run as shared-memory tiled launches (tile.cu):
@@ -2124,7 +2147,7 @@ struct Plan {
         const int nc = (int)commits.size();
         if (final) {
             tiles.clear();
-            if (rowp.ok) return;
+            if (!rows.empty()) return;
             for (int c = c_tile; c < nc;) {
                 int e = c;
                 while (e < nc && commits[e].level == commits[c].level) e++;
@@ -2136,9 +2159,10 @@ struct Plan {
             return;
         }
         c_tile = nc;
-        rowp = RowPlan{};
+        rows.clear();
+        row_level.clear();
         choose_row();
-        if (rowp.ok) return;
+        if (!rows.empty()) return;
         // opt-in (HPEZ_TILE=1): measured slower than the flow kernel on cfg2
         // so far (profiles/); kept parity-green for the tiling work ahead
         const char *ev = getenv("HPEZ_TILE");
@@ -2212,11 +2236,11 @@ static size_t plan_layout(Plan &p, char *base) {
         c.take(&p.d_errbuf, (size_t)std::max<int64_t>(p.num_codes, 1));
     }
     if (p.profile) c.take(&p.d_prof, 96);
-    if (p.rowp.ok) {
-        c.take(&p.rowp.d_cnt, (size_t)p.rowp.d.n_entries);
-        c.take(&p.rowp.d_base, (size_t)p.rowp.d.n_entries);
-        c.take(&p.rowp.d_tmp, (size_t)scan_tmp_size(p.rowp.d.n_entries));
-        c.take(&p.rowp.d_total, 4);
+    for (RowPlan &rp : p.rows) {
+        c.take(&rp.d_cnt, (size_t)rp.d.n_entries);
+        c.take(&rp.d_base, (size_t)rp.d.n_entries);
+        c.take(&rp.d_tmp, (size_t)scan_tmp_size(rp.d.n_entries));
+        c.take(&rp.d_total, 4);
     }
     if (!p.tiles.empty() && p.d.direction == HPEZ_COMPRESS) {
         char *o;
@@ -2366,8 +2390,8 @@ static int plan_setup(Plan *p, cudaStream_t st) {
         commit_ranges_kernel<<<(unsigned)p->commits.size(), 256, 0, st>>>(
             p->d_commits, (int)p->commits.size(), p->d_wbase, p->d_wn, p->d_cbase, p->d_cn);
     e = cudaGetLastError();
-    if (!e && p->rowp.ok)
-        e = row_plan_setup(p->rowp, p->table.empty() ? nullptr : p->d_table + (size_t)(p->d.n_levels - 1) * p->nblk_table, st);
+    for (size_t i = 0; i < p->rows.size() && !e; i++)
+        e = row_plan_setup(p->rows[i], p->table.empty() ? nullptr : p->d_table + (size_t)p->row_level[i] * p->nblk_table, st);
     if (e) return cuda_status(e);
     p->setup_done = true;
     return HPEZ_OK;
@@ -2664,27 +2688,29 @@ static int sweep_run(hpez_plan plan, const void *orig, void *work, void *codes, 
             if (e) return cuda_status(e);
         }
     }
-    if (p.rowp.ok) {
+    if (!p.rows.empty()) {
         const int64_t e0 = (int64_t)p.commits[p.c_tile].item_base * kItemWarps;
         if (p.d.direction == HPEZ_COMPRESS) {
             e = cudaMemsetAsync(p.d_esc_cnt + e0, 0, (size_t)(ne - e0) * sizeof(uint32_t), st);
             if (e) return cuda_status(e);
         }
-        RowRun rr{};
-        rr.orig = (const float *)orig;
-        rr.work = (float *)work;
-        rr.codes = (uint16_t *)codes;
-        rr.outl = outliers;
-        rr.outl_cap = A.outl_cap;
-        rr.esc_cnt = p.d_esc_cnt;
-        rr.esc_off = p.d_esc_off;
-        rr.flags = p.d_counters + 1;
-        rr.table = p.table.empty() ? nullptr : p.d_table + (size_t)(p.d.n_levels - 1) * p.nblk_table;
-        rr.rowbase = p.rowp.d_base;
-        rr.commits = p.d_commits;
-        rr.wbase = p.d_wbase;
-        e = row_plan_launch(p.rowp, p.d.direction, rr, st);
-        if (e) return cuda_status(e);
+        for (size_t i = 0; i < p.rows.size(); i++) {
+            RowRun rr{};
+            rr.orig = (const float *)orig;
+            rr.work = (float *)work;
+            rr.codes = (uint16_t *)codes;
+            rr.outl = outliers;
+            rr.outl_cap = A.outl_cap;
+            rr.esc_cnt = p.d_esc_cnt;
+            rr.esc_off = p.d_esc_off;
+            rr.flags = p.d_counters + 1;
+            rr.table = p.table.empty() ? nullptr : p.d_table + (size_t)p.row_level[i] * p.nblk_table;
+            rr.rowbase = p.rows[i].d_base;
+            rr.commits = p.d_commits;
+            rr.wbase = p.d_wbase;
+            e = row_plan_launch(p.rows[i], p.d.direction, rr, st);
+            if (e) return cuda_status(e);
+        }
     }
     if (p.d.direction == HPEZ_COMPRESS) {
         exclusive_scan(p.d_esc_cnt, ne, p.d_esc_off, p.d_scan_tmp, p.d_total, st);
@@ -2735,12 +2761,21 @@ int hpez_plan_tile_info(hpez_plan plan, int64_t *out, int32_t cap) {
 int hpez_plan_row_info(hpez_plan plan, int64_t *out) {
     if (!plan || !out) return HPEZ_BAD_ARGUMENT;
     const Plan &p = plan->p;
-    out[0] = p.rowp.ok ? 1 : 0;
-    out[1] = p.rowp.ok ? p.c_tile : -1;
-    out[2] = p.rowp.n_launch;
-    out[3] = p.rowp.d.n_entries;
-    out[4] = p.rowp.d.any_same;
-    out[5] = (int64_t)p.rowp.smem;
+    out[0] = (int64_t)p.rows.size();
+    out[1] = p.rows.empty() ? -1 : p.c_tile;
+    int nl = 0;
+    int64_t ent = 0, same = 0;
+    size_t smem = 0;
+    for (const RowPlan &rp : p.rows) {
+        nl += rp.n_launch;
+        ent += rp.d.n_entries;
+        same |= rp.d.any_same;
+        smem = std::max(smem, rp.smem);
+    }
+    out[2] = nl;
+    out[3] = ent;
+    out[4] = same;
+    out[5] = (int64_t)smem;
     return HPEZ_OK;
 }
 

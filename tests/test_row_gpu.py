@@ -1,11 +1,12 @@
-"""GPU parity of the row-fused finest level (csrc/row.cu) against the CPU oracle.
+"""GPU parity of the row-fused fine levels (csrc/row.cu) against the CPU oracle.
 
-The finest level of these rank-3 f32 plans is forced onto the row path
-(HPEZ_ROW_MIN=0): every multidim kernel variant as a uniform level, mixed
-per-block tables over the multidim variants with several block sizes, grids
-whose extents are not multiples of the chunk / block / 4-row phases, tiny
-error bounds (many escapes, both directions), the out-of-place compress
-entry, and the fallbacks (x extent not a multiple of 4, one-axis variants)."""
+The fine levels (strides 1, 2, 4) of these rank-3 f32 plans are forced onto
+the row path (HPEZ_ROW_MIN=0): every multidim kernel variant and the
+split-free one-axis variants as uniform levels, mixed per-block tables over
+them with several block sizes, grids whose extents are not multiples of the
+chunk / block / 4-row phases, tiny error bounds (many escapes, both
+directions), the out-of-place compress entry, and the fallbacks (x extent
+not a multiple of 4, one-axis variants with a same-level split)."""
 
 import ctypes
 
@@ -35,6 +36,8 @@ def _levels(seed, anchor, e, finest_kernel, finest_par=1):
         last = i == n - 1
         k = finest_kernel if last else int(rng.integers(0, 5))
         p = finest_par if last else int(rng.integers(0, 2))
+        if not last and i >= n - 3 and p == 0:
+            k = (0, 1, 3)[int(rng.integers(0, 3))]  # strides 2 and 4: a row-eligible one-axis variant
         order = tuple(int(a) for a in rng.permutation(3)) if p == 0 else None
         s = anchor >> (i + 1)
         out.append((s, e / min(1.5 ** (s.bit_length() - 1), 3.0), k, p, order))
@@ -47,6 +50,9 @@ def _table(seed, dims, bs, nl, finest_tags):
     tags = [p * 8 + k for p in range(len(order_candidates((0, 1, 2))) + 1) for k in range(5)]
     nb = int(np.prod([-(-d // bs) for d in dims]))
     tbl = np.array(tags, np.uint8)[rng.integers(0, len(tags), (nl, nb))]
+    ok = [t for t in tags if t < 8 or t % 8 in (0, 1, 3)]  # row-eligible tags for strides 2 and 4
+    for li in (nl - 2, nl - 3):
+        tbl[li] = np.array(ok, np.uint8)[rng.integers(0, len(ok), nb)]
     tbl[nl - 1] = np.array(finest_tags, np.uint8)[rng.integers(0, len(finest_tags), nb)]
     return tbl
 
@@ -107,50 +113,56 @@ def _force_rows(monkeypatch):
 
 
 UNIFORM = [
-    # seed, dims, finest kernel variant
-    (1, (70, 66, 92), 0),
-    (2, (65, 130, 36), 1),
-    (3, (129, 100, 56), 2),
-    (4, (40, 77, 140), 3),
-    (5, (96, 64, 64), 4),
-    (6, (33, 97, 260), 4),
-    (7, (9, 10, 12), 2),
-    (8, (67, 69, 128), 0),
-    (9, (66, 71, 132), 4),
+    # seed, dims, finest kernel variant, finest paradigm, row levels expected
+    (1, (70, 66, 92), 0, 1, 1),
+    (2, (65, 130, 36), 1, 1, 1),
+    (3, (129, 100, 56), 2, 1, 2),
+    (4, (40, 77, 140), 3, 1, 1),
+    (5, (96, 64, 64), 4, 1, 3),
+    (6, (33, 97, 272), 4, 1, 3),
+    (7, (9, 10, 12), 2, 1, 1),
+    (8, (67, 69, 128), 0, 1, 3),
+    (9, (66, 71, 132), 4, 1, 1),
+    (10, (70, 66, 96), 0, 0, 3),   # one-axis linear at the finest level
+    (11, (65, 72, 160), 1, 0, 3),  # one-axis not-a-knot
+    (12, (130, 66, 64), 3, 0, 3),  # one-axis natural
 ]
 
 
-@pytest.mark.parametrize("seed,dims,kernel", UNIFORM)
-def test_row_uniform_vs_oracle(seed, dims, kernel):
+@pytest.mark.parametrize("seed,dims,kernel,par,nrow", UNIFORM)
+def test_row_uniform_vs_oracle(seed, dims, kernel, par, nrow):
     data = _field(dims)
     e = 1e-3 * float(data.max() - data.min())
-    levels = _levels(seed, 64, e, kernel)
+    levels = _levels(seed, 64, e, kernel, par)
     md = np.random.default_rng(seed).uniform(0, 1, 3)
-    assert _row_info(data.shape, levels, md)[0] == 1
+    assert _row_info(data.shape, levels, md)[0] == nrow
     _roundtrip(data, levels, md)
 
 
 MIXED = [
-    # seed, dims, block size, finest tags
-    (11, (70, 66, 92), 16, (0, 1, 2, 3, 4)),
-    (12, (65, 130, 36), 32, (0, 1, 2, 3, 4)),
-    (13, (129, 100, 56), 8, (0, 2)),
-    (14, (40, 77, 140), 4, (0, 1, 3)),
-    (15, (96, 64, 64), 32, (0, 4)),
-    (16, (67, 69, 260), 16, (2, 4)),
-    (17, (97, 64, 128), 32, (0, 1, 2, 3, 4)),
-    (18, (66, 130, 132), 32, (0, 1, 2, 3)),
+    # seed, dims, block size, finest tags, row levels expected
+    (11, (70, 66, 92), 16, (0, 1, 2, 3, 4), 1),
+    (12, (65, 130, 36), 32, (0, 1, 2, 3, 4), 1),
+    (13, (129, 100, 56), 8, (0, 2), 2),
+    (14, (40, 77, 140), 4, (0, 1, 3), 1),
+    (15, (96, 64, 64), 32, (0, 4), 3),
+    (16, (67, 69, 272), 16, (2, 4), 3),
+    (17, (97, 64, 128), 32, (0, 1, 2, 3, 4), 3),
+    (18, (66, 130, 132), 32, (0, 1, 2, 3), 1),
+    (19, (70, 66, 96), 16, (0, 8, 17, 27, 32, 41, 48, 1, 2), 3),  # one-axis tags in the finest table
+    (20, (66, 130, 128), 32, (0, 16, 24, 40, 4), 3),
+    (21, (96, 64, 64), 8, (0, 1, 2, 3, 4), 2),                    # stride-4 blocks too small for a lane
 ]
 
 
-@pytest.mark.parametrize("seed,dims,bs,tags", MIXED)
-def test_row_mixed_vs_oracle(seed, dims, bs, tags):
+@pytest.mark.parametrize("seed,dims,bs,tags,nrow", MIXED)
+def test_row_mixed_vs_oracle(seed, dims, bs, tags, nrow):
     data = _field(dims)
     e = 1e-3 * float(data.max() - data.min())
     levels = _levels(seed, 64, e, 0)
     tbl = _table(seed, dims, bs, len(levels), tags)
     md = np.random.default_rng(seed).uniform(0, 1, 3)
-    assert _row_info(data.shape, levels, md, bs, tbl)[0] == 1
+    assert _row_info(data.shape, levels, md, bs, tbl)[0] == nrow
     _roundtrip(data, levels, md, bs, tbl)
 
 
@@ -186,10 +198,10 @@ def test_row_fallbacks():
     assert _row_info(data.shape, levels, md)[0] == 0
     _roundtrip(data, levels, md)
     data = _field((40, 44, 48))
-    levels = _levels(42, 64, e, 3, finest_par=0)  # one-axis paradigm at the finest level
+    levels = _levels(42, 64, e, 4, finest_par=0)  # one-axis paradigm with a same-level split
     assert _row_info(data.shape, levels, md)[0] == 0
     _roundtrip(data, levels, md)
     levels = _levels(43, 64, e, 0)
-    tbl = _table(43, data.shape, 16, len(levels), (0, 9, 18))  # one-axis tags in the finest table
+    tbl = _table(43, data.shape, 16, len(levels), (0, 10, 20))  # one-axis same-level tags in the finest table
     assert _row_info(data.shape, levels, md, 16, tbl)[0] == 0
     _roundtrip(data, levels, md, 16, tbl)
