@@ -556,8 +556,9 @@ def run_b200(args):
                      "frac": round(ach_c / peak, 4), "traffic": traffic,
                      "traffic_note": f"ncu dram__bytes_read+write of one compress sweep "
                                      f"(profiles/traffic_{wl_name}.json) over this run's sweep time, GB/s",
-                     "kernel": "compress sweep (coarse DSMEM cluster + flow kernel + escape scan/gather "
-                               "of one run_levels)",
+                     "kernel": "compress sweep of one run_levels (coarse DSMEM cluster + flow kernel for the "
+                               "coarse levels + row-fused launches for strides 4/2/1 + escape scan/gather); the "
+                               "stride-1 row launches are ~72% of it",
                      "algorithmic_bytes": f"{BYTES_COMPRESS} B/pt x {n} pts",
                      "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"},
         "e2e": {"value": round(world * gb / (e2e_ms / 1e3), 3), "unit": UNIT,

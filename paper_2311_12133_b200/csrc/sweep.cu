@@ -2463,10 +2463,11 @@ int32_t hpez_plan_num_launches(hpez_plan plan) {
     if (!plan) return -1;
     const Plan &p = plan->p;
     int n = 0;
-    if (!p.coarse_groups.empty()) n++;
+    if (!p.coarse_groups.empty() || p.coarse_dsmem) n++;
     if (!p.flow_order.empty()) n++;
     n += (int)p.stages.size();
     n += (int)p.tiles.size();
+    for (const RowPlan &rp : p.rows) n += rp.n_launch;  // row-fused levels (row.cu)
     n += 1;  // escape scan (single-pass look-back kernel)
     n += 1;  // escape count pre-pass (decompress) or outlier gather (compress)
     if (p.d.with_stats && p.d.direction == HPEZ_COMPRESS) n += 2;

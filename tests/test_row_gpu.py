@@ -107,6 +107,7 @@ def _roundtrip(data, levels, md, bs=0, tbl=None, oop=False):
 @pytest.fixture(autouse=True)
 def _force_rows(monkeypatch):
     monkeypatch.setenv("HPEZ_ROW_MIN", "0")
+    monkeypatch.setenv("HPEZ_ROW", "2")  # also levels that are same-level throughout (off by default)
     from paper_2311_12133_b200 import interp
     if hasattr(interp, "_PLANS"):
         interp._PLANS.clear()

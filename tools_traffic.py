@@ -18,9 +18,13 @@ def rows(path):
         unit = r["Metric Unit"]
         if r["Metric Name"] == "gpu__time_duration.sum":
             d["us"] = v / 1e3 if unit == "ns" else (v * 1e3 if unit == "ms" else v)
-        else:
+        elif r["Metric Name"].startswith("dram__"):
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
             d["dram_bytes"] = d.get("dram_bytes", 0.0) + v * scale
+        elif r["Metric Name"] == "smsp__inst_executed.sum":
+            d["warp_inst"] = v
+        elif r["Metric Name"].startswith("smsp__issue_active"):
+            d["issue_pct"] = v
     return [out[k] for k in sorted(out)]
 
 
@@ -47,7 +51,9 @@ def main():
     ks = rows(sys.argv[1])
     c, d = groups(ks)
     summ = lambda g: [{"kernel": k["kernel"][:70], "us": round(k["us"], 3),
-                       "dram_MB": round(k.get("dram_bytes", 0) / 1e6, 3)} for k in g]
+                       "dram_MB": round(k.get("dram_bytes", 0) / 1e6, 3),
+                       **({"warp_inst_M": round(k["warp_inst"] / 1e6, 2)} if "warp_inst" in k else {}),
+                       **({"issue_pct": round(k["issue_pct"], 1)} if "issue_pct" in k else {})} for k in g]
     n = int(sys.argv[4]) if len(sys.argv) > 4 else 256 * 384 * 384
     out = {"round": int(sys.argv[5]) if len(sys.argv) > 5 else 1, "source": sys.argv[3],
            "compress_sweep_kernels": summ(c),
