@@ -201,7 +201,7 @@ __device__ __forceinline__ int32_t quant_f32(const Q &q, double pred, float orig
     const double y = __dadd_rn(fabs(x), 0.5);
     double fl = floor(y);
     const double fr = __dsub_rn(y, fl);
-    if (fr < 0x1p-20 || fr > 1.0 - 0x1p-20 || y >= 0x1p20) {
+    if (fr < 0x1p-20 || fr > 1.0 - 0x1p-20) {  // |x| + 0.5 >= 2^20 fails fl < R below on either path
         x = __ddiv_rn(d, q.two_e);
         fl = floor(__dadd_rn(fabs(x), 0.5));
     }
@@ -284,25 +284,27 @@ __device__ __forceinline__ void st4(float *p, float4 v) { *reinterpret_cast<floa
 
 // Four consecutive lattice points j0 .. j0 + 3 of a row (element stride S).
 template <int S>
-__device__ __forceinline__ float4 ldl(const float *row, int j0) {
+__device__ __forceinline__ float4 ldl(const float *row, int j) {
+    const uint32_t j0 = (uint32_t)j;  // never negative: an unsigned index is one wide multiply-add
     if (S == 1) return ld4(row + j0);
     if (S == 2) {
-        const float4 a = ld4(row + 2 * j0), b = ld4(row + 2 * j0 + 4);
+        const float4 a = ld4(row + 2u * j0), b = ld4(row + 2u * j0 + 4u);
         return make_float4(a.x, a.z, b.x, b.z);
     }
-    return make_float4(row[S * j0], row[S * (j0 + 1)], row[S * (j0 + 2)], row[S * (j0 + 3)]);
+    return make_float4(row[S * j0], row[S * (j0 + 1u)], row[S * (j0 + 2u)], row[S * (j0 + 3u)]);
 }
 // Stores the components selected by MASK (stride 1: the whole 16-byte word).
 template <int S, int MASK>
-__device__ __forceinline__ void stl(float *row, int j0, float4 v) {
+__device__ __forceinline__ void stl(float *row, int j, float4 v) {
+    const uint32_t j0 = (uint32_t)j;
     if (S == 1) {
         st4(row + j0, v);
         return;
     }
     if (MASK & 1) row[S * j0] = v.x;
-    if (MASK & 2) row[S * (j0 + 1)] = v.y;
-    if (MASK & 4) row[S * (j0 + 2)] = v.z;
-    if (MASK & 8) row[S * (j0 + 3)] = v.w;
+    if (MASK & 2) row[S * (j0 + 1u)] = v.y;
+    if (MASK & 4) row[S * (j0 + 2u)] = v.z;
+    if (MASK & 8) row[S * (j0 + 3u)] = v.w;
 }
 
 // Block tags of one row: lane b holds the tag of x-block b (rows of at most 32
@@ -537,7 +539,7 @@ __device__ __forceinline__ int32_t quant_f32d(const Q &q, double pred, float ori
     const double y = __dadd_rn(fabs(x), 0.5);
     double fl = floor(y);
     const double fr = __dsub_rn(y, fl);
-    if (fr < 0x1p-20 || fr > 1.0 - 0x1p-20 || y >= 0x1p20) {
+    if (fr < 0x1p-20 || fr > 1.0 - 0x1p-20) {  // |x| + 0.5 >= 2^20 fails fl < R below on either path
         x = __ddiv_rn(d, q.two_e);
         fl = floor(__dadd_rn(fabs(x), 0.5));
     }
@@ -596,18 +598,19 @@ __device__ __forceinline__ void process_rowN(const RowDesc &D, const RowRun &A, 
     const uint32_t lt = (1u << lane) - 1u;
     const int nch = (Lx + 127) >> 7;
     const RowTags T = row_tags(D, A, z, y, lane);
-    // chunks whose blocks all carry tag 0: one bit per chunk
-    uint32_t plain = 0;
+    // chunks whose blocks all carry tag 0: bit b of nz set = block b has another tag
+    uint32_t nz = 0xffffffffu;
+    int bpc = 0;  // blocks per chunk (0: no per-chunk test, every chunk general unless nz == 0)
     if (lin_ok) {
         if (!T.table) {
-            plain = T.const_tag == 0 ? 0xffffffffu : 0u;
-        } else if (T.in_reg && T.bsh <= 7) {
-            const uint32_t nz = __ballot_sync(0xffffffffu, T.reg != 0);
-            const int bpc = 128 >> T.bsh;  // blocks per chunk
-            for (int c = 0; c < nch && c * bpc < 32; c++)
-                if (((nz >> (c * bpc)) & (bpc >= 32 ? 0xffffffffu : ((1u << bpc) - 1u))) == 0) plain |= 1u << c;
+            nz = T.const_tag == 0 ? 0u : 0xffffffffu;
+        } else if (T.in_reg && T.bsh <= 7 && (Lx >> T.bsh) <= 32) {
+            nz = __ballot_sync(0xffffffffu, T.reg != 0);
+            bpc = 128 >> T.bsh;
         }
     }
+    const uint32_t bmask = bpc >= 32 || bpc == 0 ? 0xffffffffu : ((1u << bpc) - 1u);
+    auto is_plain = [&](int c) { return ((nz >> (bpc ? c * bpc : 0)) & bmask) == 0; };
     float p_e0 = 0.0f, p_e2 = 0.0f;  // stage E results of the previous chunk (for the finished word)
     for (int it = 0; it <= nch; it++) {
         float n_e0 = 0.0f, n_e2 = 0.0f;
@@ -624,7 +627,7 @@ __device__ __forceinline__ void process_rowN(const RowDesc &D, const RowRun &A, 
                     prefetch_l1(pp[t] + S * (x0 + 128));
                 }
             }
-            if ((plain >> it) & 1u) {
+            if (is_plain(it)) {
                 const int nact = min(32, (Lx - (it << 7)) >> 2);
                 uint16_t *__restrict__ cp = A.codes + baseEA + 2 * lane;
                 baseEA += 2 * nact;
@@ -736,7 +739,7 @@ __device__ __forceinline__ void process_rowN(const RowDesc &D, const RowRun &A, 
             const int h = x0 >> 1;
             const bool r4 = x0 + 4 <= Lx - 1;
             uint16_t *__restrict__ cp = cO + 2 * (((it - 1) << 5) + lane);
-            if ((plain >> (it - 1)) & 1u) {
+            if (is_plain(it - 1)) {
                 if (act) {
                     float oy = 0.0f, ow = 0.0f;
                     int32_t c1 = 0, c3 = 0;
