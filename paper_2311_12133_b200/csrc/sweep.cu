@@ -315,7 +315,10 @@ __device__ __forceinline__ const PredDev *mixed_member(const SweepArgs &A, const
                                                        bool *member) {
     const GridDev &g = A.g;
     int64_t b = 0;
-    for (int a = 0; a < g.rank; a++) b += (int64_t)(coord[a] / g.block_size) * g.bstr[a];
+    if (g.bs_log2 >= 0)
+        for (int a = 0; a < g.rank; a++) b += (int64_t)(coord[a] >> g.bs_log2) * g.bstr[a];
+    else
+        for (int a = 0; a < g.rank; a++) b += (int64_t)(coord[a] / g.block_size) * g.bstr[a];
     const int tag = A.table[(int64_t)cm.level * g.nblk + b];
     const TagInfo &ti = A.tags[cm.tag_off + A.slots[cm.slot_off + tag]];
     const int sp = ti.split;

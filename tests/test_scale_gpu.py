@@ -7,7 +7,9 @@ test_container.py:96) including the int32-code variant (radius > 32768).
 
 These are the size-dependent schedules the small fixtures cannot reach:
 diagonal item bands, npos/(2*SMs) item sizing, the coarse-cluster cutoff,
-512^3 index arithmetic and the mixed (block-table) fast path."""
+512^3 index arithmetic, the mixed (block-table) fast path and the row kernel of
+the fine levels (csrc/row.cu: cfg4 mostly tag-0 chunks, cfg5 56 % cubic /
+same-level blocks at strides 1, 2, 4; eps 1e-5 thousands of escapes)."""
 
 import numpy as np
 import pytest
@@ -77,7 +79,7 @@ def test_cfg2_full_size_vs_oracle():
     assert n == f.size - 4 * 6 * 6
 
 
-@pytest.mark.parametrize("cfg_id,eps,dims", [(3, 1e-4, None), (4, 1e-3, None)])
+@pytest.mark.parametrize("cfg_id,eps,dims", [(3, 1e-4, None), (4, 1e-3, None), (5, 1e-3, None), (4, 1e-5, None)])
 def test_tuned_block_table_full_size_vs_oracle(cfg_id, eps, dims):
     f, cfg, levels, eb = _tuned(cfg_id, eps, dims)
     assert cfg.predictor == "interp"
