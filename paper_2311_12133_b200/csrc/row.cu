@@ -445,10 +445,10 @@ __device__ __noinline__ void process_row0_lag(const RowDesc &D, const RowRun &A,
     }
 }
 
-// Rows whose blocks carry no same-level variant have a single pass: both
-// x-odd points of a lane from its own 16-byte word and the next coarse value
-// (shuffled from the next lane); only rows that cross a same-level block
-// take the two-pass routine above.
+// Rows whose blocks carry no same-level variant have a single pass: the four
+// x-odd points of a lane from its own two 16-byte words and the next coarse
+// value (shuffled from the next lane); only rows that cross a same-level
+// block take the two-pass routine above.
 template <int DIR, int S>
 __device__ __forceinline__ void process_row0(const RowDesc &D, const RowRun &A, const Q &q, int z, int y, double *rb,
                                              int lane) {
@@ -474,44 +474,60 @@ __device__ __forceinline__ void process_row0(const RowDesc &D, const RowRun &A, 
     const bool oop = DIR == HPEZ_COMPRESS && A.orig != A.work;
     const int64_t baseA = D.level_base + A.rowbase[D.segA[2] + rowidx];
     const int cmA = D.commitA[2];
-    const int nch = (Lx + 127) >> 7;
     const RowTags T = row_tags(D, A, z, y, lane);
+    // eight lattice points (two words, four x-odd points) per lane and iteration
+    const int nch = (Lx + 255) >> 8;
     for (int it = 0; it < nch; it++) {
-        const int x0 = (it << 7) + (lane << 2);
-        const bool act = x0 < Lx;
-        const int tag = tag_at(T, x0, act);
-        const int fi = tag_fam(tag);
-        const bool lin = !__any_sync(0xffffffffu, fi != 0);
-        float4 w = make_float4(0, 0, 0, 0), o = w;
-        int32_t c1 = 0, c3 = 0;
-        const int64_t ci = baseA + 2 * ((it << 5) + lane);
-        if (act) {
-            w = ldl<S>(wrow, x0);
-            if (oop) o = ldl<S>(orow, x0);
-            else o = w;
+        const int x0 = (it << 8) + (lane << 3);
+        const bool actA = x0 < Lx, actB = x0 + 4 < Lx;
+        const int tagA = tag_at(T, x0, actA), tagB = tag_at(T, x0 + 4, actB);
+        const int fA = tag_fam(tagA), fB = tag_fam(tagB);
+        const bool lin = !__any_sync(0xffffffffu, (fA | fB) != 0);
+        float4 wa = make_float4(0, 0, 0, 0), wb = wa, oa = wa, ob = wa;
+        int32_t c1 = 0, c3 = 0, c5 = 0, c7 = 0;
+        const int64_t ci = baseA + 4 * ((it << 5) + lane);
+        if (actA) {
+            wa = ldl<S>(wrow, x0);
+            oa = oop ? ldl<S>(orow, x0) : wa;
             if (DIR == HPEZ_DECOMPRESS) load_codes2(A.codes + ci, &c1, &c3);
         }
-        const bool r4 = x0 + 4 <= Lx - 1;
-        double pr1, pr3;
+        if (actB) {
+            wb = ldl<S>(wrow, x0 + 4);
+            ob = oop ? ldl<S>(orow, x0 + 4) : wb;
+            if (DIR == HPEZ_DECOMPRESS) load_codes2(A.codes + ci + 2, &c5, &c7);
+        }
+        const bool r4 = x0 + 4 <= Lx - 1, r8 = x0 + 8 <= Lx - 1;
+        double pr1, pr3, pr5, pr7;
         if (lin) {
-            float w4 = __shfl_down_sync(0xffffffffu, w.x, 1);
-            if (lane == 31 && act && r4) w4 = wrow[S * (x0 + 4)];
-            const double d0 = (double)w.x, d2 = (double)w.z;
+            float w8 = __shfl_down_sync(0xffffffffu, wa.x, 1);
+            if (lane == 31 && r8) w8 = wrow[S * (uint32_t)(x0 + 8)];
+            const double d0 = (double)wa.x, d2 = (double)wa.z, d4 = (double)wb.x, d6 = (double)wb.z;
             pr1 = DA(DM(0.5, d0), DM(0.5, d2));
-            pr3 = r4 ? DA(DM(0.5, d2), DM(0.5, (double)w4)) : DM(1.0, d2);
+            pr3 = r4 ? DA(DM(0.5, d2), DM(0.5, d4)) : DM(1.0, d2);
+            pr5 = DA(DM(0.5, d4), DM(0.5, d6));
+            pr7 = r8 ? DA(DM(0.5, d6), DM(0.5, (double)w8)) : DM(1.0, d6);
         } else {
             float4 wp = make_float4(0, 0, 0, 0), wn = wp;
-            if (act && x0 >= 4) wp = ldl<S>(wrow, x0 - 4);
-            if (act && r4) wn = ldl<S>(wrow, x0 + 4);
-            const double d0 = (double)w.x, d2 = (double)w.z, d4 = (double)wn.x;
-            pr1 = pred_gen(fi, (double)wp.z, d0, d2, d4, true, x0 >= 2 && r4, x0 + 1, Lx);
-            pr3 = pred_gen(fi, d0, d2, d4, (double)wn.z, r4, x0 + 6 <= Lx - 1, x0 + 3, Lx);
+            if (actA && x0 >= 4) wp = ldl<S>(wrow, x0 - 4);
+            if (r8) wn = ldl<S>(wrow, x0 + 8);
+            const double d0 = (double)wa.x, d2 = (double)wa.z, d4 = (double)wb.x, d6 = (double)wb.z;
+            const double d8 = (double)wn.x, d10 = (double)wn.z;
+            pr1 = pred_gen(fA, (double)wp.z, d0, d2, d4, true, x0 >= 2 && r4, x0 + 1, Lx);
+            pr3 = pred_gen(fA, d0, d2, d4, d6, r4, x0 + 6 <= Lx - 1, x0 + 3, Lx);
+            pr5 = pred_gen(fB, d2, d4, d6, d8, true, r8, x0 + 5, Lx);
+            pr7 = pred_gen(fB, d4, d6, d8, d10, r8, x0 + 10 <= Lx - 1, x0 + 7, Lx);
         }
-        if (act) {
+        if (actA) {
             float r1, r3;
-            point2<DIR>(q, A, pr1, pr3, o.y, o.w, &c1, &c3, cmA, z, y, x0 + 1, x0 + 3, ci, &r1, &r3);
+            point2<DIR>(q, A, pr1, pr3, oa.y, oa.w, &c1, &c3, cmA, z, y, x0 + 1, x0 + 3, ci, &r1, &r3);
             if (DIR == HPEZ_COMPRESS) store_codes2(A.codes + ci, c1, c3);
-            stl<S, 10>(A.work + rowoff, x0, make_float4(w.x, r1, w.z, r3));
+            stl<S, 10>(A.work + rowoff, x0, make_float4(wa.x, r1, wa.z, r3));
+        }
+        if (actB) {
+            float r5, r7;
+            point2<DIR>(q, A, pr5, pr7, ob.y, ob.w, &c5, &c7, cmA, z, y, x0 + 5, x0 + 7, ci + 2, &r5, &r7);
+            if (DIR == HPEZ_COMPRESS) store_codes2(A.codes + ci + 2, c5, c7);
+            stl<S, 10>(A.work + rowoff, x0 + 4, make_float4(wb.x, r5, wb.z, r7));
         }
     }
 }
