@@ -40,8 +40,16 @@
 
 namespace hpez {
 
+// CTAs per SM of the three instantiations (measured sweep, cfg4 / cfg5): rows with one of z, y odd 4
+// (64 registers), (z even, y even) rows and (z odd, y odd) rows 3 (80 registers)
 #ifndef HPEZ_ROW_OCC
-#define HPEZ_ROW_OCC 3
+#define HPEZ_ROW_OCC 4
+#endif
+#ifndef HPEZ_ROW_OCC0
+#define HPEZ_ROW_OCC0 3
+#endif
+#ifndef HPEZ_ROW_OCC8
+#define HPEZ_ROW_OCC8 3
 #endif
 #ifndef HPEZ_ROW_PF
 #define HPEZ_ROW_PF 1
@@ -849,10 +857,12 @@ __device__ __forceinline__ void process_rowN(const RowDesc &D, const RowRun &A, 
     }
 }
 
-template <int DIR, int S>
-__global__ void __launch_bounds__(kRowThreads, HPEZ_ROW_OCC) row_kernel(const __grid_constant__ RowDesc D,
-                                                                       const __grid_constant__ RowRun A,
-                                                                       const __grid_constant__ RowLaunch L) {
+// RTM: the row types a launch holds (bit 0: (z even, y even); bits 1-2: one of z, y odd;
+// bit 3: both odd), so each instantiation carries -- and is register-allocated for -- only
+// its own routines.
+template <int DIR, int S, int RTM>
+__global__ void __launch_bounds__(kRowThreads, RTM == 1 ? HPEZ_ROW_OCC0 : RTM == 8 ? HPEZ_ROW_OCC8 : HPEZ_ROW_OCC)
+    row_kernel(const __grid_constant__ RowDesc D, const __grid_constant__ RowRun A, const __grid_constant__ RowLaunch L) {
     extern __shared__ double s_rb[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *rb = s_rb + (size_t)warp * ((D.L[2] >> 1) + 4);
@@ -870,13 +880,16 @@ __global__ void __launch_bounds__(kRowThreads, HPEZ_ROW_OCC) row_kernel(const __
         const int rr = r < n0 ? r : r - n0;
         const int iz = rr / S0.ny, iy = rr - iz * S0.ny;
         const int z = S0.z0 + iz * S0.zs, y = S0.y0 + iy * S0.ys;
-        switch (S0.rt * 2 + S0.brow) {
-        case 0: process_row0<DIR, S>(D, A, q, z, y, rb, lane); break;
-        case 2: process_rowN<DIR, S, 1, false>(D, A, q, z, y, rb, lane); break;
-        case 3: process_rowN<DIR, S, 1, true>(D, A, q, z, y, rb, lane); break;
-        case 4: process_rowN<DIR, S, 2, false>(D, A, q, z, y, rb, lane); break;
-        case 5: process_rowN<DIR, S, 2, true>(D, A, q, z, y, rb, lane); break;
-        default: process_rowN<DIR, S, 3, false>(D, A, q, z, y, rb, lane); break;
+        const int kind = S0.rt * 2 + S0.brow;
+        if (RTM == 1) {
+            process_row0<DIR, S>(D, A, q, z, y, rb, lane);
+        } else if (RTM == 6) {
+            if (kind == 2) process_rowN<DIR, S, 1, false>(D, A, q, z, y, rb, lane);
+            else if (kind == 3) process_rowN<DIR, S, 1, true>(D, A, q, z, y, rb, lane);
+            else if (kind == 4) process_rowN<DIR, S, 2, false>(D, A, q, z, y, rb, lane);
+            else process_rowN<DIR, S, 2, true>(D, A, q, z, y, rb, lane);
+        } else {
+            process_rowN<DIR, S, 3, false>(D, A, q, z, y, rb, lane);
         }
         __syncwarp();
     }
@@ -1072,11 +1085,16 @@ cudaError_t row_plan_setup(RowPlan &p, const uint8_t *d_table_level, cudaStream_
 
 typedef void (*row_fn)(const RowDesc, const RowRun, const RowLaunch);
 
+template <int DIR, int S>
+static row_fn pick_rtm(int rtm) {
+    return rtm == 1 ? row_kernel<DIR, S, 1> : rtm == 6 ? row_kernel<DIR, S, 6> : row_kernel<DIR, S, 8>;
+}
+template <int DIR>
+static row_fn pick_row(int s, int rtm) {
+    return s == 1 ? pick_rtm<DIR, 1>(rtm) : s == 2 ? pick_rtm<DIR, 2>(rtm) : pick_rtm<DIR, 4>(rtm);
+}
+
 cudaError_t row_plan_launch(const RowPlan &p, int dir, const RowRun &r, cudaStream_t st) {
-    const bool c = dir == HPEZ_COMPRESS;
-    row_fn f = p.d.s == 1   ? (c ? row_kernel<HPEZ_COMPRESS, 1> : row_kernel<HPEZ_DECOMPRESS, 1>)
-               : p.d.s == 2 ? (c ? row_kernel<HPEZ_COMPRESS, 2> : row_kernel<HPEZ_DECOMPRESS, 2>)
-                            : (c ? row_kernel<HPEZ_COMPRESS, 4> : row_kernel<HPEZ_DECOMPRESS, 4>);
     static int sms = 0;
     if (!sms) {
         int dev = 0;
@@ -1084,12 +1102,15 @@ cudaError_t row_plan_launch(const RowPlan &p, int dir, const RowRun &r, cudaStre
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (sms <= 0) sms = 148;
     }
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, p.threads, p.smem) != cudaSuccess || occ < 1) occ = 1;
     for (int i = 0; i < p.n_launch; i++) {
         const RowLaunch &l = p.launch[i];
         if (l.total <= 0) continue;
+        const int rt = l.s[0].rt;
+        const int rtm = rt == 0 ? 1 : rt == 3 ? 8 : 6;
+        row_fn f = dir == HPEZ_COMPRESS ? pick_row<HPEZ_COMPRESS>(p.d.s, rtm) : pick_row<HPEZ_DECOMPRESS>(p.d.s, rtm);
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, p.threads, p.smem) != cudaSuccess || occ < 1) occ = 1;
         const int grid = std::max(1, std::min((l.total + kRowWarps - 1) / kRowWarps, occ * sms));
         f<<<grid, p.threads, p.smem, st>>>(p.d, r, l);
     }
