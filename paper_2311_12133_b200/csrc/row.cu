@@ -857,8 +857,8 @@ __device__ __forceinline__ void process_rowN(const RowDesc &D, const RowRun &A, 
     }
 }
 
-// RTM: the row types a launch holds (bit 0: (z even, y even); bits 1-2: one of z, y odd;
-// bit 3: both odd), so each instantiation carries -- and is register-allocated for -- only
+// RTM: the row types a launch holds (1: (z even, y even); 6 / 7: one of z, y odd, first-pass /
+// second-pass rows; 8: both odd), so each instantiation carries -- and is register-allocated for -- only
 // its own routines.
 template <int DIR, int S, int RTM>
 __global__ void __launch_bounds__(kRowThreads, RTM == 1 ? HPEZ_ROW_OCC0 : RTM == 8 ? HPEZ_ROW_OCC8 : HPEZ_ROW_OCC)
@@ -883,10 +883,11 @@ __global__ void __launch_bounds__(kRowThreads, RTM == 1 ? HPEZ_ROW_OCC0 : RTM ==
         const int kind = S0.rt * 2 + S0.brow;
         if (RTM == 1) {
             process_row0<DIR, S>(D, A, q, z, y, rb, lane);
-        } else if (RTM == 6) {
+        } else if (RTM == 6) {  // one of z, y odd, no second-pass lanes in these rows
             if (kind == 2) process_rowN<DIR, S, 1, false>(D, A, q, z, y, rb, lane);
-            else if (kind == 3) process_rowN<DIR, S, 1, true>(D, A, q, z, y, rb, lane);
-            else if (kind == 4) process_rowN<DIR, S, 2, false>(D, A, q, z, y, rb, lane);
+            else process_rowN<DIR, S, 2, false>(D, A, q, z, y, rb, lane);
+        } else if (RTM == 7) {  // one of z, y odd, second same-level pass rows
+            if (kind == 3) process_rowN<DIR, S, 1, true>(D, A, q, z, y, rb, lane);
             else process_rowN<DIR, S, 2, true>(D, A, q, z, y, rb, lane);
         } else {
             process_rowN<DIR, S, 3, false>(D, A, q, z, y, rb, lane);
@@ -1087,7 +1088,7 @@ typedef void (*row_fn)(const RowDesc, const RowRun, const RowLaunch);
 
 template <int DIR, int S>
 static row_fn pick_rtm(int rtm) {
-    return rtm == 1 ? row_kernel<DIR, S, 1> : rtm == 6 ? row_kernel<DIR, S, 6> : row_kernel<DIR, S, 8>;
+    return rtm == 1 ? row_kernel<DIR, S, 1> : rtm == 6 ? row_kernel<DIR, S, 6> : rtm == 7 ? row_kernel<DIR, S, 7> : row_kernel<DIR, S, 8>;
 }
 template <int DIR>
 static row_fn pick_row(int s, int rtm) {
@@ -1106,7 +1107,7 @@ cudaError_t row_plan_launch(const RowPlan &p, int dir, const RowRun &r, cudaStre
         const RowLaunch &l = p.launch[i];
         if (l.total <= 0) continue;
         const int rt = l.s[0].rt;
-        const int rtm = rt == 0 ? 1 : rt == 3 ? 8 : 6;
+        const int rtm = rt == 0 ? 1 : rt == 3 ? 8 : (l.s[0].brow ? 7 : 6);
         row_fn f = dir == HPEZ_COMPRESS ? pick_row<HPEZ_COMPRESS>(p.d.s, rtm) : pick_row<HPEZ_DECOMPRESS>(p.d.s, rtm);
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
         int occ = 0;
