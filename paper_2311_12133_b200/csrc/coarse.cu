@@ -384,6 +384,16 @@ bool coarse_dsmem_build(const GridDev &g, const CommitDev *cms, const int *group
     for (int k = 0; k < n; k++) ncc = std::max<int64_t>(ncc, D.c[k].code_base + (int64_t)D.c[k].cnt[0] * D.c[k].cnt[1] * D.c[k].cnt[2]);
     for (int k = 0; k < n; k++) if (D.c[k].code_base < 0) return false;
     if (ncc >= (1ll << 30)) return false;
+    // the in-kernel outlier ranking counts zero codes over [0, n_cc): the coarse commits' code
+    // ranges must tile that stream prefix exactly, in order
+    {
+        int64_t pos = 0;
+        for (int k = 0; k < n; k++) {
+            if (D.c[k].code_base != pos) return false;
+            pos += (int64_t)D.c[k].cnt[0] * D.c[k].cnt[1] * D.c[k].cnt[2];
+        }
+        if (pos != ncc) return false;
+    }
     D.n_cc = (int32_t)ncc;
     const size_t smem = (size_t)D.P * D.L[1] * D.L[2] * (sizeof(double) + sizeof(uint16_t)) + 16 +
                         3 * kCoarseMaxCommits * sizeof(int32_t) +
