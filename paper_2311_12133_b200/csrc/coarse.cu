@@ -14,6 +14,7 @@
 // written to global memory once.
 #include <algorithm>
 #include <cstdlib>
+#include <utility>
 #include <vector>
 
 #include "stencil.cuh"
@@ -387,10 +388,14 @@ bool coarse_dsmem_build(const GridDev &g, const CommitDev *cms, const int *group
     // the in-kernel outlier ranking counts zero codes over [0, n_cc): the coarse commits' code
     // ranges must tile that stream prefix exactly, in order
     {
+        std::vector<std::pair<int64_t, int64_t>> rng;  // (first code, codes) of every coarse commit
+        for (int k = 0; k < n; k++)
+            rng.push_back({D.c[k].code_base, (int64_t)D.c[k].cnt[0] * D.c[k].cnt[1] * D.c[k].cnt[2]});
+        std::sort(rng.begin(), rng.end());
         int64_t pos = 0;
-        for (int k = 0; k < n; k++) {
-            if (D.c[k].code_base != pos) return false;
-            pos += (int64_t)D.c[k].cnt[0] * D.c[k].cnt[1] * D.c[k].cnt[2];
+        for (const auto &r : rng) {
+            if (r.first != pos) return false;
+            pos += r.second;
         }
         if (pos != ncc) return false;
     }
