@@ -142,7 +142,7 @@ __device__ __forceinline__ double pred_gen(int fi, double m3, double a, double b
 }
 
 // Same-level 1-D row (second pass of a split class) over c-3 .. c+3.
-__device__ __noinline__ double pred_same(int nat, double m3, double m2, double m1, double p1, double p2, double p3,
+__device__ __forceinline__ double pred_same(int nat, double m3, double m2, double m1, double p1, double p2, double p3,
                                          int c, int E) {
     if (nat) {
         const double x[6] = {m3, m2, m1, p1, p2, p3};
