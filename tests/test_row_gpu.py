@@ -206,3 +206,31 @@ def test_row_fallbacks():
     tbl = _table(43, data.shape, 16, len(levels), (0, 10, 20))  # one-axis same-level tags in the finest table
     assert _row_info(data.shape, levels, md, 16, tbl)[0] == 0
     _roundtrip(data, levels, md, 16, tbl)
+
+
+TAGS_OK = (0, 1, 2, 3, 4, 8, 9, 11, 16, 17, 19, 24, 32, 40, 41, 48, 51)  # multidim + split-free one-axis tags
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_row_random_configs(case):
+    """Randomised geometry / table / bound draws (tools_fuzz_rows.py ran 420 of
+    these against the oracle): odd and even z, y extents, x extents 12..276,
+    block sizes 0/4/8/16/32, tag subsets, both compress entries."""
+    rng = np.random.default_rng(9000 + case)
+    dims = (int(rng.integers(9, 140)), int(rng.integers(9, 140)), int(rng.integers(3, 70)) * 4)
+    bs = int(rng.choice([0, 4, 8, 16, 32]))
+    eps = float(rng.choice([1e-2, 1e-3, 1e-4, 1e-6]))
+    seed = int(rng.integers(0, 1 << 30))
+    k, par = int(rng.integers(0, 5)), int(rng.integers(0, 2))
+    if par == 0 and k in (2, 4):
+        k = 1
+    data = _field(dims)
+    if rng.integers(0, 2):
+        data = (data + rng.standard_normal(dims).astype(np.float32) * 0.2).astype(np.float32)
+    e = eps * float(data.max() - data.min())
+    levels = _levels(seed, 64, e, k, par)
+    sub = [int(t) for t in rng.choice(TAGS_OK, size=int(rng.integers(1, 7)), replace=False)]
+    tbl = _table(seed, dims, bs, len(levels), sub) if bs else None
+    md = rng.uniform(0, 1, 3)
+    assert _row_info(data.shape, levels, md, bs, tbl)[0] >= 1
+    _roundtrip(data, levels, md, bs, tbl, oop=bool(rng.integers(0, 2)))
