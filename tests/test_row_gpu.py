@@ -153,6 +153,8 @@ MIXED = [
     (19, (70, 66, 96), 16, (0, 8, 17, 27, 32, 41, 48, 1, 2), 3),  # one-axis tags in the finest table
     (20, (66, 130, 128), 32, (0, 16, 24, 40, 4), 3),
     (21, (96, 64, 64), 8, (0, 1, 2, 3, 4), 2),                    # stride-4 blocks too small for a lane
+    (22, (20, 24, 1280), 32, (0, 1, 2, 3, 4), 2),                 # 40 x-blocks: tags read per chunk, 10 chunks per row
+    (23, (18, 20, 1924), 16, (0, 2, 4), 1),                       # 121 x-blocks, a partial last chunk
 ]
 
 
